@@ -1,0 +1,158 @@
+/* tk.h — C ABI of the B200-native top-k sparsified gradient aggregation library (libtk.so).
+ *
+ * Implements the data-parallel hot path of "Towards Scalable Distributed Training of Deep
+ * Learning on Public Cloud Clusters" (Shi et al., arXiv 2010.10458, MLSys'21), CommLib §3
+ * (PAPER.md P:127-266):
+ *   error feedback (acc = g + r)                     — BASELINE.json north_star (not in the paper)
+ *   MSTopK approximate top-k, Algorithm 1            — P:148-188
+ *   compaction into ascending (index, value) pairs   — Alg. 1 l.25-29, P:180-185 (reading Q11)
+ *   sparse All-Gather of (kappa, iota)               — §3.2, Eq. 3
+ *   rank-ordered index accumulation (decompress)     — Alg. 2 l.15-20
+ *   residual write-back of the unsent mass           — BASELINE.json north_star
+ *   HiTopKComm (m x n virtual nodes), Algorithm 2    — P:203-248
+ * "Q<n>" refers to the numbered readings of silent/ambiguous passages in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *   - Pointers to vectors are DEVICE pointers (cudaMalloc / torch CUDA tensors), 16-byte aligned,
+ *     unless the name ends in _host.  The caller owns every vector it passes; libtk owns only its
+ *     scratch (allocated in tk_init, freed in tk_destroy).
+ *   - All device work is enqueued on the stream given to tk_init, asynchronously w.r.t. the host,
+ *     except tk_init, tk_get_stats, tk_step_host and tk_destroy, which synchronise that stream.
+ *   - Every call returns a tk_status; no C++ exception crosses the ABI.  Arguments are validated
+ *     before anything is launched.  Details of the last failure: tk_last_error(ctx).
+ *   - Results are a pure function of (inputs, config, step counter, rank): independent of grid
+ *     size, SM count and timing.  A context is single-stream and not thread-safe.
+ *   - Gradients are fp32 (Eq. 3 bills 4-byte FP32 elements).  d < 2^32 (u32 indices).
+ */
+#ifndef TK_H_
+#define TK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tk_ctx tk_ctx;
+typedef void* tk_stream_t; /* a cudaStream_t (0 = legacy default stream) */
+
+typedef enum tk_status {
+  TK_OK = 0,
+  TK_ERR_INVALID_ARG = 1, /* NULL / misaligned pointer, d == 0 or d >= 2^32, rho not in (0,1],
+                             N not in [1,52], rank >= P, aliasing buffers                    */
+  TK_ERR_RANGE = 2,       /* explicit k not in [1, d] (segment length for HiTopKComm)          */
+  TK_ERR_CONFIG = 3,      /* P % n != 0, d % n != 0, NCCL unique id missing for P > 1          */
+  TK_ERR_NONFINITE = 4,   /* NaN/Inf met in acc (precondition, Q24); sticky, reported by the
+                             next tk_get_stats                                                 */
+  TK_ERR_CUDA = 5,        /* CUDA runtime error; text in tk_last_error                        */
+  TK_ERR_NCCL = 6,        /* NCCL error; text in tk_last_error                                 */
+  TK_ERR_STATE = 7,       /* wrong call order (e.g. tk_sparse_allgather with P == 1 comm absent)*/
+  TK_ERR_NOMEM = 8        /* device allocation of scratch failed                              */
+} tk_status;
+
+enum { TK_RAND_SEEDED = 0, TK_RAND_FIRST = 1 };   /* Alg. 1 l.27 window start (Q10)           */
+enum { TK_STEP4_DENSE = 0, TK_STEP4_SPARSE = 1 }; /* HiTopKComm step 4: Alg. 2 l.21-23 vs Eq.10*/
+
+typedef struct tk_config {
+  uint64_t d;              /* gradient length (the paper's d)                           */
+  double rho;              /* density, 0 < rho <= 1                                    */
+  uint64_t k;              /* 0: k = max(1, floor(rho*d)) (Q13); else explicit, 1 <= k <= d     */
+  uint32_t n_iters;        /* MSTopK N, the number of threshold samplings (Alg. 1 input), 1..52 */
+  uint32_t nranks;         /* P workers (one process per GPU)                                  */
+  uint32_t rank;           /* this process's rank in [0, P)                                    */
+  uint32_t group_size;     /* n: 1 = flat NaiveAG; >1 = HiTopKComm with m = P/n */
+  uint64_t seed;           /* seed of the window RNG (Q10)                                     */
+  uint32_t rand_mode;      /* TK_RAND_SEEDED (default) or TK_RAND_FIRST (rand = 0)             */
+  uint32_t error_feedback; /* 1: acc = g + r, r' = acc with sent entries := +0.0 (Q14);
+                              0: MSTopK runs on g itself and r is ignored (may be NULL)         */
+  uint32_t step4;          /* HiTopKComm step 4 mode (TK_STEP4_DENSE or TK_STEP4_SPARSE)       */
+  uint32_t levels_per_pass;/* bisection levels resolved per count pass over the data (1..4;
+                              0 = default 3).  Result bits do not depend on it.               */
+  int32_t device;          /* CUDA device ordinal to use (-1 = current)                        */
+} tk_config;
+
+/* Snapshot of the last compression's MSTopK control block (for parity checks). */
+typedef struct tk_stats {
+  double mean;             /* a-bar, canonical fp64 pairwise mean of |acc| (Alg. 1 l.2, Q3)    */
+  uint32_t max_bits;       /* bits of u = max |acc| (Alg. 1 l.3)                               */
+  uint32_t n_trials;       /* = N                                                              */
+  double ratio[52];        /* per trial: ratio (Alg. 1 l.8)                                    */
+  double thres[52];        /*            thres (l.9, fp64, Q4)                                 */
+  uint32_t key[52];        /*            bits of the smallest fp32 >= thres                    */
+  uint32_t nnz[52];        /*            count_nonzero(a >= thres) (l.10)                      */
+  uint64_t k, k1, k2;      /* Alg. 1 l.5 state after the loop                                  */
+  double thres1, thres2;   /* l.6 state after the loop (0 when never set)                      */
+  uint32_t key1, key2;     /* integer keys of thres1 / thres2 (0x7F800000 / 0 when unset)      */
+  uint32_t thres1_set, thres2_set;
+  uint64_t len2;           /* len(iota2) (l.26)                                                */
+  uint64_t rand_start;     /* rand (l.27)                                                      */
+  uint64_t step;           /* step counter used for this compression's RNG draw               */
+  uint32_t nonfinite;      /* 1 if a NaN/Inf was seen (sticky)                                 */
+} tk_stats;
+
+/* k = max(1, floor(rho * d)) in fp64 (Q13).  Host-only, pure.  0 on invalid input. */
+uint64_t tk_k(uint64_t d, double rho);
+
+/* Rank 0 creates the 128-byte NCCL unique id that every rank passes to tk_init (P > 1). */
+tk_status tk_get_unique_id(uint8_t uid[128]);
+
+/* Collective over all P ranks when P > 1 (NCCL communicator bootstrap from uid; HiTopKComm also
+ * splits row (size n) and column (size m) communicators).  uid may be NULL iff P == 1.
+ * On success *out owns all scratch; release with tk_destroy. */
+tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, tk_ctx** out);
+
+/* MSTopK compression of one rank (Alg. 1 + error feedback), flat mode only.
+ *   g   [d]  in     gradient (never written)
+ *   r   [d]  in/out residual r -> r' (error_feedback = 1); ignored when error_feedback = 0
+ *   idx [k]  out    selected indices iota, strictly ascending (Q11)
+ *   val [k]  out    kappa = acc[iota], bit-copied (Q12)
+ * g must not alias r, idx or val. */
+tk_status tk_compress(tk_ctx* ctx, const float* g, float* r, uint32_t* idx, float* val);
+
+/* Sparse All-Gather: gathered [P][2k] u32, rank-major, each rank's chunk laid out as
+ * [idx k | bits(val) k] (Q15).  idx/val are this rank's tk_compress outputs.  Collective. */
+tk_status tk_sparse_allgather(tk_ctx* ctx, const uint32_t* idx, const float* val, uint32_t* gathered);
+
+/* Rank-ordered index accumulation (Alg. 2 l.15-20): out = +0^d; for p = 0..nchunks-1 in order:
+ * out[idx_p] += val_p in fp32 round-to-nearest (Q16).  gathered is [nchunks][2k] as above, each
+ * chunk's indices strictly ascending and < d (violations: memory-safe, result unspecified).
+ * nchunks in [1, 4096]; out has d elements (flat) or d/n (HiTopKComm segment).  A larger
+ * nchunks than any previous call grows an internal table (synchronises the stream). */
+tk_status tk_decompress(tk_ctx* ctx, const uint32_t* gathered, uint32_t nchunks, float* out);
+
+/* One whole iteration (flat: compress -> all-gather -> decompress; HiTopKComm: Alg. 2 steps 1-4).
+ *   g   [d]            in      local gradient
+ *   r   [d] or [d/n]   in/out  residual (flat: d; HiTopKComm: the segment length d/n, Q22)
+ *   out [d]            out     aggregated sparse gradient, bitwise identical on every rank
+ *   gathered           out     optional (NULL = internal): flat [P][2k]; HiTopKComm [m][2k~]
+ * Increments the step counter after enqueueing. */
+tk_status tk_step(tk_ctx* ctx, const float* g, float* r, float* out, uint32_t* gathered);
+
+/* tk_step with HOST buffers (end-to-end path): copies g_host (pinned or pageable) to the device,
+ * runs tk_step with a context-owned device residual (state carried across calls; zero at init),
+ * and copies the P*2k gathered pairs (flat) back to gathered_host and, if out_host != NULL, the
+ * dense aggregate back to out_host.  Synchronises the context stream. */
+tk_status tk_step_host(tk_ctx* ctx, const float* g_host, uint32_t* gathered_host, float* out_host);
+
+/* Copy the control block of the last compression to *st (synchronises the stream). */
+tk_status tk_get_stats(tk_ctx* ctx, tk_stats* st);
+
+/* Set the step counter used by the next compression's window draw (resume; Q10). */
+tk_status tk_set_step(tk_ctx* ctx, uint64_t step);
+
+/* Sizes derived at init: k (flat) or k~ (HiTopKComm), segment length, P, m, n. */
+tk_status tk_query(const tk_ctx* ctx, uint64_t* k, uint64_t* seg_len, uint32_t* nranks, uint32_t* m,
+                   uint32_t* n);
+
+/* Number of kernel launches libtk enqueued on the context stream since init (evidence counter). */
+uint64_t tk_launch_count(const tk_ctx* ctx);
+
+tk_status tk_destroy(tk_ctx* ctx);
+const char* tk_status_string(tk_status s);
+const char* tk_last_error(const tk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TK_H_ */

@@ -1,0 +1,278 @@
+"""paper_2010_10458_b200 — B200-native top-k sparsified gradient aggregation (arXiv 2010.10458).
+
+Thin Python binding over the C ABI of ``libtk.so`` (include/tk.h): argument marshalling only.
+Every step of the hot path — error feedback, MSTopK (Alg. 1), compaction, the sparse
+All-Gather (NCCL, issued inside libtk), rank-ordered decompression and HiTopKComm (Alg. 2) —
+runs in libtk's sm_100a kernels.  There is no CPU fallback: importing this package without a
+built ``libtk.so`` raises, and every call fails loudly on a non-CUDA tensor.
+
+PyTorch supplies device memory, the CUDA stream and the ``torch.distributed`` bootstrap of the
+NCCL unique id (plumbing only).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch  # loads the venv's libnccl.so.2 first; libtk links the same soname
+
+__all__ = ["Context", "TkError", "k_from_density", "unique_id", "broadcast_unique_id", "lib_path", "STATUS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libtk.so")
+
+STATUS = {0: "TK_OK", 1: "TK_ERR_INVALID_ARG", 2: "TK_ERR_RANGE", 3: "TK_ERR_CONFIG", 4: "TK_ERR_NONFINITE",
+          5: "TK_ERR_CUDA", 6: "TK_ERR_NCCL", 7: "TK_ERR_STATE", 8: "TK_ERR_NOMEM"}
+NMAX = 52
+
+
+class TkError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_uint64), ("rho", ctypes.c_double), ("k", ctypes.c_uint64),
+                ("n_iters", ctypes.c_uint32), ("nranks", ctypes.c_uint32), ("rank", ctypes.c_uint32),
+                ("group_size", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("rand_mode", ctypes.c_uint32),
+                ("error_feedback", ctypes.c_uint32), ("step4", ctypes.c_uint32),
+                ("levels_per_pass", ctypes.c_uint32), ("device", ctypes.c_int32)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("mean", ctypes.c_double), ("max_bits", ctypes.c_uint32), ("n_trials", ctypes.c_uint32),
+                ("ratio", ctypes.c_double * NMAX), ("thres", ctypes.c_double * NMAX),
+                ("key", ctypes.c_uint32 * NMAX), ("nnz", ctypes.c_uint32 * NMAX),
+                ("k", ctypes.c_uint64), ("k1", ctypes.c_uint64), ("k2", ctypes.c_uint64),
+                ("thres1", ctypes.c_double), ("thres2", ctypes.c_double),
+                ("key1", ctypes.c_uint32), ("key2", ctypes.c_uint32),
+                ("thres1_set", ctypes.c_uint32), ("thres2_set", ctypes.c_uint32),
+                ("len2", ctypes.c_uint64), ("rand_start", ctypes.c_uint64), ("step", ctypes.c_uint64),
+                ("nonfinite", ctypes.c_uint32)]
+
+
+# Every symbol include/tk.h declares (checked by tests/test_abi.py).
+EXPORTS = ["tk_k", "tk_get_unique_id", "tk_init", "tk_compress", "tk_sparse_allgather", "tk_decompress",
+           "tk_step", "tk_step_host", "tk_get_stats", "tk_set_step", "tk_query", "tk_launch_count",
+           "tk_destroy", "tk_status_string", "tk_last_error"]
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"libtk.so not built at {_LIB_PATH}: run `python -m paper_2010_10458_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, U32, U64, I32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+    sig = {
+        "tk_k": (U64, [U64, ctypes.c_double]),
+        "tk_get_unique_id": (I32, [ctypes.c_char_p]),
+        "tk_init": (I32, [ctypes.POINTER(_Config), ctypes.c_char_p, P, ctypes.POINTER(P)]),
+        "tk_compress": (I32, [P, P, P, P, P]),
+        "tk_sparse_allgather": (I32, [P, P, P, P]),
+        "tk_decompress": (I32, [P, P, U32, P]),
+        "tk_step": (I32, [P, P, P, P, P]),
+        "tk_step_host": (I32, [P, P, P, P]),
+        "tk_get_stats": (I32, [P, ctypes.POINTER(_Stats)]),
+        "tk_set_step": (I32, [P, U64]),
+        "tk_query": (I32, [P, ctypes.POINTER(U64), ctypes.POINTER(U64), ctypes.POINTER(U32),
+                           ctypes.POINTER(U32), ctypes.POINTER(U32)]),
+        "tk_launch_count": (U64, [P]),
+        "tk_destroy": (I32, [P]),
+        "tk_status_string": (ctypes.c_char_p, [I32]),
+        "tk_last_error": (ctypes.c_char_p, [P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def k_from_density(d: int, rho: float) -> int:
+    """k = max(1, floor(rho*d)) (reading Q13), computed by libtk."""
+    k = int(_lib.tk_k(int(d), float(rho)))
+    if k == 0:
+        raise ValueError("invalid d / rho")
+    return k
+
+
+def unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = _lib.tk_get_unique_id(buf)
+    if st != 0:
+        raise TkError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0 creates the NCCL unique id; torch.distributed broadcasts the 128 bytes."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(unique_id()), dtype=torch.uint8))
+    if dist.get_backend(group) == "nccl":
+        tc = t.cuda()
+        dist.broadcast(tc, src=0, group=group)
+        t = tc.cpu()
+    else:
+        dist.broadcast(t, src=0, group=group)
+    return bytes(t.tolist())
+
+
+def _ptr(t, name, dtype):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (libtk has no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class Stats:
+    mean: float
+    max_bits: int
+    trials: list  # (ratio, thres, key, nnz)
+    k: int
+    k1: int
+    k2: int
+    thres1: float
+    thres2: float
+    thres1_set: bool
+    thres2_set: bool
+    key1: int
+    key2: int
+    len2: int
+    rand: int
+    step: int
+    nonfinite: bool
+
+
+class Context:
+    """One rank's libtk context (tk_init).  ``d, rho, n_iters`` follow the paper's statement of
+    the problem (x in R^d, k = rho*d, N samplings, P workers, m x n for HiTopKComm)."""
+
+    def __init__(self, d: int, rho: float = 0.001, n_iters: int = 10, *, k: int = 0, nranks: int = 1, rank: int = 0,
+                 group_size: int = 1, seed: int = 0, rand_mode: str = "seeded", error_feedback: bool = True,
+                 step4: str = "dense", levels_per_pass: int = 0, device: int | None = None, uid: bytes | None = None,
+                 stream: torch.cuda.Stream | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libtk needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+        dev = torch.cuda.current_device() if device is None else int(device)
+        self.device = torch.device("cuda", dev)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        cfg = _Config(d=int(d), rho=float(rho), k=int(k), n_iters=int(n_iters), nranks=int(nranks), rank=int(rank),
+                      group_size=int(group_size), seed=int(seed) & ((1 << 64) - 1),
+                      rand_mode={"seeded": 0, "first": 1}[rand_mode], error_feedback=1 if error_feedback else 0,
+                      step4={"dense": 0, "sparse": 1}[step4], levels_per_pass=int(levels_per_pass), device=dev)
+        self._ctx = ctypes.c_void_p()
+        if nranks > 1 and uid is None:
+            raise ValueError("nranks > 1 needs the NCCL unique id (broadcast_unique_id())")
+        st = _lib.tk_init(ctypes.byref(cfg), uid, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(self._ctx))
+        if st != 0:
+            raise TkError(st, "tk_init failed (" + _lib.tk_status_string(st).decode() + ")")
+        k_, L, P, m, n = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        self._check(_lib.tk_query(self._ctx, ctypes.byref(k_), ctypes.byref(L), ctypes.byref(P), ctypes.byref(m),
+                                  ctypes.byref(n)))
+        self.d, self.k, self.seg_len = int(d), k_.value, L.value
+        self.nranks, self.m, self.n, self.rank = P.value, m.value, n.value, int(rank)
+        self.error_feedback = bool(error_feedback)
+
+    # -------------------------------------------------------------------------------------
+    def _check(self, st):
+        if st != 0:
+            raise TkError(st, _lib.tk_last_error(self._ctx).decode(errors="replace"))
+
+    def _empty(self, n, dtype):
+        return torch.empty(n, dtype=dtype, device=self.device)
+
+    @property
+    def chunks(self) -> int:
+        return self.nranks if self.n == 1 else self.m
+
+    def compress(self, g, r=None, idx=None, val=None):
+        """tk_compress: returns (idx uint32-as-int32 tensor, val float32 tensor)."""
+        idx = self._empty(self.k, torch.int32) if idx is None else idx
+        val = self._empty(self.k, torch.float32) if val is None else val
+        self._check(_lib.tk_compress(self._ctx, _ptr(g, "g", torch.float32),
+                                     _ptr(r, "r", torch.float32) if self.error_feedback else None,
+                                     _ptr(idx, "idx", torch.int32), _ptr(val, "val", torch.float32)))
+        return idx, val
+
+    def sparse_allgather(self, idx, val, gathered=None):
+        gathered = self._empty(self.chunks * 2 * self.k, torch.int32) if gathered is None else gathered
+        self._check(_lib.tk_sparse_allgather(self._ctx, _ptr(idx, "idx", torch.int32), _ptr(val, "val", torch.float32),
+                                             _ptr(gathered, "gathered", torch.int32)))
+        return gathered
+
+    def decompress(self, gathered, nchunks=None, out=None):
+        n_out = self.d if self.n == 1 else self.seg_len
+        out = self._empty(n_out, torch.float32) if out is None else out
+        nch = self.chunks if nchunks is None else int(nchunks)
+        self._check(_lib.tk_decompress(self._ctx, _ptr(gathered, "gathered", torch.int32), nch,
+                                       _ptr(out, "out", torch.float32)))
+        return out
+
+    def step(self, g, r=None, out=None, gathered=None):
+        """tk_step: one whole iteration; returns the dense aggregated gradient."""
+        out = self._empty(self.d, torch.float32) if out is None else out
+        self._check(_lib.tk_step(self._ctx, _ptr(g, "g", torch.float32),
+                                 _ptr(r, "r", torch.float32) if self.error_feedback else None,
+                                 _ptr(out, "out", torch.float32),
+                                 _ptr(gathered, "gathered", torch.int32) if gathered is not None else None))
+        return out
+
+    def step_host(self, g_host, gathered_host=None, out_host=None):
+        """tk_step_host: HOST buffers in/out (numpy or pinned CPU tensors); synchronous."""
+        def hp(a):
+            if a is None:
+                return None
+            if isinstance(a, torch.Tensor):
+                assert not a.is_cuda and a.is_contiguous()
+                return ctypes.c_void_p(a.data_ptr())
+            return ctypes.c_void_p(a.ctypes.data)
+        self._check(_lib.tk_step_host(self._ctx, hp(g_host), hp(gathered_host), hp(out_host)))
+        return gathered_host, out_host
+
+    def stats(self) -> Stats:
+        s = _Stats()
+        st = _lib.tk_get_stats(self._ctx, ctypes.byref(s))
+        if st not in (0, 4):
+            self._check(st)
+        trials = [(s.ratio[i], s.thres[i], s.key[i], s.nnz[i]) for i in range(s.n_trials)]
+        return Stats(mean=s.mean, max_bits=s.max_bits, trials=trials, k=s.k, k1=s.k1, k2=s.k2, thres1=s.thres1,
+                     thres2=s.thres2, thres1_set=bool(s.thres1_set), thres2_set=bool(s.thres2_set), key1=s.key1,
+                     key2=s.key2, len2=s.len2, rand=s.rand_start, step=s.step, nonfinite=bool(s.nonfinite))
+
+    def set_step(self, step: int):
+        self._check(_lib.tk_set_step(self._ctx, int(step)))
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.tk_launch_count(self._ctx))
+
+    def close(self):
+        if self._ctx:
+            _lib.tk_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

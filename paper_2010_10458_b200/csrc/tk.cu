@@ -1,0 +1,479 @@
+// tk.cu — libtk runtime: the C ABI declared in include/tk.h.
+//
+// Owns the per-context scratch (tile partials, per-tile trial counts, prefix sums, control
+// block, packed send/receive buffers), the NCCL communicators (world; for HiTopKComm also the
+// row comm of the n GPUs of a virtual node and the column comm of the m GPUs with the same
+// position), and the launch sequence of one iteration.  Everything is enqueued on the caller's
+// stream with no host synchronisation inside an iteration, so a whole tk_step is capturable in
+// a CUDA graph by the caller.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "tk.h"
+#include "tk_kernels.cuh"
+
+using namespace tk;
+
+struct tk_ctx {
+  tk_config cfg;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t P = 1, m = 1, n = 1, rank = 0;
+  uint32_t row_pos = 0, col_pos = 0;  // j = rank % n (position in the node), i = rank / n (node)
+  uint64_t d = 0, L = 0, k = 0;       // L = d / n (segment length); k = k (flat) or k~ (HiTopK)
+  uint32_t ntiles = 0;                // tiles of the vector MSTopK runs on (length L)
+  uint32_t ntiles_d = 0;              // tiles of d
+  uint32_t levels = 3, npass = 0;
+  int lev_sched[NMAX];
+  double* tile_sum = nullptr;
+  uint32_t* tile_max = nullptr;
+  uint16_t* tile_counts = nullptr;
+  uint32_t* pre1 = nullptr;
+  uint32_t* pre2 = nullptr;
+  Ctrl* ctrl = nullptr;
+  uint32_t* send = nullptr;      // [2k]
+  uint32_t* recv = nullptr;      // flat: [P][2k]; HiTopK: [m][2k~]
+  uint32_t* recv_row = nullptr;  // HiTopK sparse step 4: [n][m][2k~]
+  uint32_t* starts = nullptr;    // [max chunks][ntiles_d + 1]
+  uint32_t max_chunks = 1;
+  float* seg = nullptr;          // HiTopK step-1 output [L]
+  float* h_g = nullptr;          // tk_step_host device staging
+  float* h_r = nullptr;
+  float* h_out = nullptr;
+  ncclComm_t world = nullptr, row = nullptr, col = nullptr;
+  uint64_t step = 0;
+  uint64_t launches = 0;
+  uint32_t nonfinite_sticky = 0;
+  char err[512] = {0};
+};
+
+namespace {
+
+tk_status fail(tk_ctx* c, tk_status s, const char* fmt, ...) {
+  if (c) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof(c->err), fmt, ap);
+    va_end(ap);
+  }
+  return s;
+}
+
+#define TK_CUDA(ctx, expr)                                                                     \
+  do {                                                                                         \
+    cudaError_t e_ = (expr);                                                                   \
+    if (e_ != cudaSuccess) return fail((ctx), TK_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TK_NCCL(ctx, expr)                                                                     \
+  do {                                                                                         \
+    ncclResult_t r_ = (expr);                                                                  \
+    if (r_ != ncclSuccess) return fail((ctx), TK_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+
+#define TK_TRY(expr)               \
+  do {                             \
+    tk_status s_ = (expr);         \
+    if (s_ != TK_OK) return s_;    \
+  } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+tk_status check_launch(tk_ctx* c, const char* what) {
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, TK_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  return TK_OK;
+}
+
+SearchParams search_params(const tk_ctx* c) {
+  SearchParams sp;
+  sp.n = c->L;
+  sp.k = c->k;
+  sp.ntiles = c->ntiles;
+  sp.n_iters = c->cfg.n_iters;
+  sp.levels = c->levels;
+  sp.rank = c->rank;
+  sp.seed = c->cfg.seed;
+  sp.rand_mode = c->cfg.rand_mode;
+  return sp;
+}
+
+template <int T>
+tk_status launch_count(tk_ctx* c, const float* acc, const SearchParams& sp, int pass, int lev, int next_lev) {
+  k_count<T><<<c->ntiles, THREADS, 0, c->stream>>>(acc, c->ctrl, sp, c->tile_counts, pass, lev, next_lev);
+  return check_launch(c, "k_count");
+}
+
+// MSTopK on a vector of length L (= c->L) with error feedback: g (+ r) -> idx/val.
+tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, float* val) {
+  const bool ef = c->cfg.error_feedback != 0;
+  const SearchParams sp = search_params(c);
+  if (ef) {
+    k_ef_stats<true><<<c->ntiles, THREADS, 0, c->stream>>>(g, r, c->L, c->tile_sum, c->tile_max);
+  } else {
+    k_ef_stats<false><<<c->ntiles, THREADS, 0, c->stream>>>(g, nullptr, c->L, c->tile_sum, c->tile_max);
+  }
+  TK_TRY(check_launch(c, "k_ef_stats"));
+  const float* acc = ef ? r : g;
+  k_finalize<<<1, FIN_THREADS, 0, c->stream>>>(c->tile_sum, c->tile_max, c->ctrl, sp, c->step, c->lev_sched[0]);
+  TK_TRY(check_launch(c, "k_finalize"));
+  for (uint32_t p = 0; p < c->npass; ++p) {
+    const int lev = c->lev_sched[p];
+    const int next = (p + 1 < c->npass) ? c->lev_sched[p + 1] : 0;
+    switch (lev) {
+      case 1: TK_TRY(launch_count<1>(c, acc, sp, (int)p, lev, next)); break;
+      case 2: TK_TRY(launch_count<3>(c, acc, sp, (int)p, lev, next)); break;
+      case 3: TK_TRY(launch_count<7>(c, acc, sp, (int)p, lev, next)); break;
+      default: TK_TRY(launch_count<15>(c, acc, sp, (int)p, lev, next)); break;
+    }
+  }
+  k_scan<<<1, SCAN_THREADS, 0, c->stream>>>(c->ctrl, sp, c->tile_counts, c->pre1, c->pre2);
+  TK_TRY(check_launch(c, "k_scan"));
+  k_select<<<c->ntiles, THREADS, 0, c->stream>>>(acc, c->ctrl, sp, c->pre1, c->pre2, idx, val, ef ? r : nullptr);
+  TK_TRY(check_launch(c, "k_select"));
+  return TK_OK;
+}
+
+// Rank-ordered decompression of nchunks chunks of kk pairs into out[0, len).
+tk_status decompress_impl(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, uint64_t kk, uint64_t len,
+                          float* out, bool clear_starts) {
+  const uint32_t nt = (uint32_t)((len + TILE - 1) / TILE);
+  if (clear_starts)
+    TK_CUDA(c, cudaMemsetAsync(c->starts, 0, sizeof(uint32_t) * (size_t)nchunks * (nt + 1), c->stream));
+  const uint64_t tot = (uint64_t)nchunks * (kk + 1);
+  const uint32_t blocks = (uint32_t)std::min<uint64_t>((tot + 255) / 256, 148ull * 16);
+  k_tile_ranges<<<blocks, 256, 0, c->stream>>>(gathered, nchunks, kk, len, nt, c->starts);
+  TK_TRY(check_launch(c, "k_tile_ranges"));
+  k_decompress<<<nt, THREADS, 0, c->stream>>>(gathered, nchunks, kk, len, nt, c->starts, out);
+  TK_TRY(check_launch(c, "k_decompress"));
+  return TK_OK;
+}
+
+template <typename T>
+tk_status dev_alloc(tk_ctx* c, T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * count);
+  if (e != cudaSuccess) return fail(c, TK_ERR_NOMEM, "cudaMalloc(%zu B): %s", sizeof(T) * count, cudaGetErrorString(e));
+  return TK_OK;
+}
+
+void free_all(tk_ctx* c) {
+  void* ptrs[] = {c->tile_sum, c->tile_max, c->tile_counts, c->pre1, c->pre2, c->ctrl, c->send, c->recv,
+                  c->recv_row, c->starts, c->seg, c->h_g, c->h_r, c->h_out};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->row) ncclCommDestroy(c->row);
+  if (c->col) ncclCommDestroy(c->col);
+  if (c->world) ncclCommDestroy(c->world);
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t tk_k(uint64_t d, double rho) {
+  if (d == 0 || !(rho > 0.0) || rho > 1.0) return 0;
+  const double prod = rho * (double)d;  // fl64(rho * d)
+  const uint64_t k = (uint64_t)std::floor(prod);
+  return k < 1 ? 1 : k;
+}
+
+tk_status tk_get_unique_id(uint8_t uid[128]) {
+  if (!uid) return TK_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return TK_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  memcpy(uid, &id, 128);
+  return TK_OK;
+}
+
+tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, tk_ctx** out) {
+  if (!cfg || !out) return TK_ERR_INVALID_ARG;
+  *out = nullptr;
+  const tk_config& k = *cfg;
+  if (k.d == 0 || k.d >= (1ull << 32)) return TK_ERR_INVALID_ARG;
+  if (k.k == 0 && (!(k.rho > 0.0) || k.rho > 1.0)) return TK_ERR_INVALID_ARG;
+  if (k.n_iters < 1 || k.n_iters > (uint32_t)NMAX) return TK_ERR_INVALID_ARG;
+  if (k.nranks < 1 || k.rank >= k.nranks) return TK_ERR_INVALID_ARG;
+  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 4) return TK_ERR_INVALID_ARG;
+  const uint32_t n = k.group_size == 0 ? 1 : k.group_size;
+  if (k.nranks % n != 0) return TK_ERR_CONFIG;
+  if (k.d % n != 0) return TK_ERR_CONFIG;
+  if (k.nranks > 1 && !uid) return TK_ERR_CONFIG;
+  const uint64_t L = k.d / n;
+  uint64_t kk = k.k;
+  if (kk == 0) kk = tk_k(L, k.rho);
+  if (kk < 1 || kk > L) return TK_ERR_RANGE;
+
+  tk_ctx* c = new (std::nothrow) tk_ctx();
+  if (!c) return TK_ERR_NOMEM;
+  c->cfg = k;
+  c->cfg.group_size = n;
+  c->P = k.nranks;
+  c->n = n;
+  c->m = k.nranks / n;
+  c->rank = k.rank;
+  c->row_pos = k.rank % n;
+  c->col_pos = k.rank / n;
+  c->d = k.d;
+  c->L = L;
+  c->k = kk;
+  c->stream = reinterpret_cast<cudaStream_t>(stream);
+  c->ntiles = (uint32_t)((L + TILE - 1) / TILE);
+  c->ntiles_d = (uint32_t)((k.d + TILE - 1) / TILE);
+  c->levels = k.levels_per_pass == 0 ? 3 : k.levels_per_pass;
+  for (uint32_t done = 0; done < k.n_iters;) {
+    const uint32_t lev = std::min(c->levels, k.n_iters - done);
+    c->lev_sched[c->npass++] = (int)lev;
+    done += lev;
+  }
+  auto bail = [&](tk_status s) {
+    free_all(c);
+    // keep no context on failure; report through the return code only
+    delete c;
+    return s;
+  };
+  if (k.device >= 0) {
+    if (cudaSetDevice(k.device) != cudaSuccess) return bail(TK_ERR_CUDA);
+  }
+  cudaGetDevice(&c->device);
+  tk_status s;
+  if ((s = dev_alloc(c, &c->tile_sum, c->ntiles)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->tile_max, c->ntiles)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->tile_counts, (size_t)c->npass * TMAX * c->ntiles)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->pre1, c->ntiles)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->pre2, c->ntiles)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->ctrl, 1)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->send, 2 * kk)) != TK_OK) return bail(s);
+  const uint32_t chunks_recv = (n == 1) ? c->P : c->m;
+  if ((s = dev_alloc(c, &c->recv, (size_t)chunks_recv * 2 * kk)) != TK_OK) return bail(s);
+  c->max_chunks = std::max<uint32_t>(c->P, 1);
+  if ((s = dev_alloc(c, &c->starts, (size_t)c->max_chunks * (c->ntiles_d + 1))) != TK_OK) return bail(s);
+  if (n > 1) {
+    if ((s = dev_alloc(c, &c->seg, L)) != TK_OK) return bail(s);
+    if (k.step4 == TK_STEP4_SPARSE)
+      if ((s = dev_alloc(c, &c->recv_row, (size_t)n * c->m * 2 * kk)) != TK_OK) return bail(s);
+  }
+  if (cudaMemset(c->ctrl, 0, sizeof(Ctrl)) != cudaSuccess) return bail(TK_ERR_CUDA);
+  if (c->P > 1) {
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    if (ncclCommInitRank(&c->world, (int)c->P, id, (int)c->rank) != ncclSuccess) return bail(TK_ERR_NCCL);
+    if (n > 1) {
+      if (ncclCommSplit(c->world, (int)(c->rank / n), (int)c->rank, &c->row, nullptr) != ncclSuccess)
+        return bail(TK_ERR_NCCL);
+      if (c->m > 1 &&
+          ncclCommSplit(c->world, (int)(c->rank % n), (int)c->rank, &c->col, nullptr) != ncclSuccess)
+        return bail(TK_ERR_NCCL);
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(TK_ERR_CUDA);
+  *out = c;
+  return TK_OK;
+}
+
+tk_status tk_compress(tk_ctx* c, const float* g, float* r, uint32_t* idx, float* val) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (c->n != 1) return fail(c, TK_ERR_STATE, "tk_compress is the flat-mode entry point (group_size == 1)");
+  const bool ef = c->cfg.error_feedback != 0;
+  if (!g || !idx || !val || (ef && !r)) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(g) || (ef && !aligned16(r))) return fail(c, TK_ERR_INVALID_ARG, "g/r must be 16-byte aligned");
+  if ((const void*)g == (const void*)r) return fail(c, TK_ERR_INVALID_ARG, "g aliases r");
+  TK_TRY(compress_impl(c, g, ef ? r : nullptr, idx, val));
+  return TK_OK;
+}
+
+tk_status tk_sparse_allgather(tk_ctx* c, const uint32_t* idx, const float* val, uint32_t* gathered) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (!idx || !val || !gathered) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  const size_t kb = sizeof(uint32_t) * c->k;
+  const uint32_t* src = c->send;
+  if ((const void*)val == (const void*)(idx + c->k)) {
+    src = idx;  // caller already holds the packed [idx | val] layout
+  } else {
+    TK_CUDA(c, cudaMemcpyAsync(c->send, idx, kb, cudaMemcpyDeviceToDevice, c->stream));
+    TK_CUDA(c, cudaMemcpyAsync(c->send + c->k, val, kb, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (c->P == 1) {
+    if (src != gathered) TK_CUDA(c, cudaMemcpyAsync(gathered, src, 2 * kb, cudaMemcpyDeviceToDevice, c->stream));
+    return TK_OK;
+  }
+  ncclComm_t comm = (c->n == 1) ? c->world : c->col;
+  if (!comm) return fail(c, TK_ERR_STATE, "no communicator for the sparse all-gather");
+  TK_NCCL(c, ncclAllGather(src, gathered, 2 * c->k, ncclUint32, comm, c->stream));
+  return TK_OK;
+}
+
+tk_status tk_decompress(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, float* out) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (!gathered || !out) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(out)) return fail(c, TK_ERR_INVALID_ARG, "out must be 16-byte aligned");
+  if (nchunks < 1 || nchunks > 4096) return fail(c, TK_ERR_INVALID_ARG, "nchunks must lie in [1, 4096]");
+  if (nchunks > c->max_chunks) {  // grow the range table (synchronises the stream)
+    TK_CUDA(c, cudaStreamSynchronize(c->stream));
+    TK_CUDA(c, cudaFree(c->starts));
+    c->starts = nullptr;
+    TK_TRY(dev_alloc(c, &c->starts, (size_t)nchunks * (c->ntiles_d + 1)));
+    c->max_chunks = nchunks;
+  }
+  const uint64_t len = (c->n == 1) ? c->d : c->L;
+  return decompress_impl(c, gathered, nchunks, c->k, len, out, true);
+}
+
+tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gathered) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  const bool ef = c->cfg.error_feedback != 0;
+  if (!g || !out || (ef && !r)) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(g) || !aligned16(out) || (ef && !aligned16(r))) return fail(c, TK_ERR_INVALID_ARG, "misaligned pointer");
+  if ((const void*)g == (const void*)r || (const void*)g == (const void*)out || (const void*)r == (const void*)out)
+    return fail(c, TK_ERR_INVALID_ARG, "g, r and out must not alias");
+  uint32_t* send = c->send;
+  const size_t kb = sizeof(uint32_t) * c->k;
+  if (c->n == 1) {
+    // flat NaiveAG: compress -> one packed all-gather -> rank-ordered decompress
+    TK_TRY(compress_impl(c, g, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k)));
+    uint32_t* gat = gathered ? gathered : c->recv;
+    if (c->P > 1) {
+      TK_NCCL(c, ncclAllGather(send, gat, 2 * c->k, ncclUint32, c->world, c->stream));
+    } else {
+      TK_CUDA(c, cudaMemcpyAsync(gat, send, 2 * kb, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    TK_TRY(decompress_impl(c, gat, c->P, c->k, c->d, out, false));
+  } else {
+    // HiTopKComm (Alg. 2).  Step 1: intra-node reduce-scatter of g (Eq. 4).
+    TK_NCCL(c, ncclReduceScatter(g, c->seg, c->L, ncclFloat32, ncclSum, c->row, c->stream));
+    // Step 2: MSTopK on the segment with k~ (Eq. 5), error feedback on the segment residual.
+    TK_TRY(compress_impl(c, c->seg, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k)));
+    // Step 3: inter-node all-gather among the m GPUs at the same position j (Eq. 6) ...
+    uint32_t* gat = gathered ? gathered : c->recv;
+    if (c->m > 1) {
+      TK_NCCL(c, ncclAllGather(send, gat, 2 * c->k, ncclUint32, c->col, c->stream));
+    } else {
+      TK_CUDA(c, cudaMemcpyAsync(gat, send, 2 * kb, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    float* my_seg = out + (size_t)c->row_pos * c->L;
+    if (c->cfg.step4 == TK_STEP4_DENSE) {
+      // ... accumulated in group order into this GPU's segment, then step 4: dense intra-node
+      // all-gather of the segments (Alg. 2 l.21-23), in place.
+      TK_TRY(decompress_impl(c, gat, c->m, c->k, c->L, my_seg, false));
+      TK_NCCL(c, ncclAllGather(my_seg, out, c->L, ncclFloat32, c->row, c->stream));
+    } else {
+      // step 4 sparse (Eq. 10): all-gather the m*k~ gathered pairs of every segment, then every
+      // GPU accumulates all segments itself (same per-element order -> identical bits).
+      TK_NCCL(c, ncclAllGather(gat, c->recv_row, (size_t)c->m * 2 * c->k, ncclUint32, c->row, c->stream));
+      for (uint32_t j = 0; j < c->n; ++j)
+        TK_TRY(decompress_impl(c, c->recv_row + (size_t)j * c->m * 2 * c->k, c->m, c->k, c->L,
+                               out + (size_t)j * c->L, false));
+    }
+  }
+  c->step++;
+  return TK_OK;
+}
+
+tk_status tk_step_host(tk_ctx* c, const float* g_host, uint32_t* gathered_host, float* out_host) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (!g_host) return fail(c, TK_ERR_INVALID_ARG, "null g_host");
+  if (!c->h_g) {
+    TK_TRY(dev_alloc(c, &c->h_g, c->d));
+    TK_TRY(dev_alloc(c, &c->h_r, c->L));
+    TK_TRY(dev_alloc(c, &c->h_out, c->d));
+    TK_CUDA(c, cudaMemsetAsync(c->h_r, 0, sizeof(float) * c->L, c->stream));
+  }
+  TK_CUDA(c, cudaMemcpyAsync(c->h_g, g_host, sizeof(float) * c->d, cudaMemcpyHostToDevice, c->stream));
+  TK_TRY(tk_step(c, c->h_g, c->h_r, c->h_out, nullptr));
+  if (gathered_host) {
+    const size_t chunks = (c->n == 1) ? c->P : c->m;
+    TK_CUDA(c, cudaMemcpyAsync(gathered_host, c->recv, sizeof(uint32_t) * chunks * 2 * c->k, cudaMemcpyDeviceToHost,
+                               c->stream));
+  }
+  if (out_host)
+    TK_CUDA(c, cudaMemcpyAsync(out_host, c->h_out, sizeof(float) * c->d, cudaMemcpyDeviceToHost, c->stream));
+  TK_CUDA(c, cudaStreamSynchronize(c->stream));
+  return TK_OK;
+}
+
+tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
+  if (!c || !st) return TK_ERR_INVALID_ARG;
+  Ctrl h;
+  TK_CUDA(c, cudaMemcpyAsync(&h, c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, c->stream));
+  TK_CUDA(c, cudaStreamSynchronize(c->stream));
+  memset(st, 0, sizeof(*st));
+  st->mean = h.abar;
+  st->max_bits = h.umax_bits;
+  st->n_trials = h.it;
+  for (uint32_t i = 0; i < h.it && i < (uint32_t)NMAX; ++i) {
+    st->ratio[i] = h.ratio_log[i];
+    st->thres[i] = h.thres_log[i];
+    st->key[i] = h.key_log[i];
+    st->nnz[i] = h.nnz_log[i];
+  }
+  st->k = c->k;
+  st->k1 = h.k1;
+  st->k2 = h.k2;
+  st->thres1 = h.thres1;
+  st->thres2 = h.thres2;
+  st->thres1_set = h.prov1 >= 0;
+  st->thres2_set = h.prov2 >= 0;
+  st->key1 = st->thres1_set ? h.key1 : INF_BITS;
+  st->key2 = st->thres2_set ? h.key2 : 0u;
+  st->len2 = h.len2;
+  st->rand_start = h.rand;
+  st->step = h.step;
+  c->nonfinite_sticky |= h.nonfinite;
+  st->nonfinite = c->nonfinite_sticky;
+  if (c->nonfinite_sticky) return fail(c, TK_ERR_NONFINITE, "non-finite value in acc (precondition, Q24)");
+  return TK_OK;
+}
+
+tk_status tk_set_step(tk_ctx* c, uint64_t step) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  c->step = step;
+  return TK_OK;
+}
+
+tk_status tk_query(const tk_ctx* c, uint64_t* k, uint64_t* seg_len, uint32_t* nranks, uint32_t* m, uint32_t* n) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (k) *k = c->k;
+  if (seg_len) *seg_len = c->L;
+  if (nranks) *nranks = c->P;
+  if (m) *m = c->m;
+  if (n) *n = c->n;
+  return TK_OK;
+}
+
+uint64_t tk_launch_count(const tk_ctx* c) { return c ? c->launches : 0; }
+
+tk_status tk_destroy(tk_ctx* c) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_all(c);
+  delete c;
+  return TK_OK;
+}
+
+const char* tk_status_string(tk_status s) {
+  switch (s) {
+    case TK_OK: return "ok";
+    case TK_ERR_INVALID_ARG: return "invalid argument";
+    case TK_ERR_RANGE: return "k out of range";
+    case TK_ERR_CONFIG: return "invalid configuration";
+    case TK_ERR_NONFINITE: return "non-finite input";
+    case TK_ERR_CUDA: return "CUDA error";
+    case TK_ERR_NCCL: return "NCCL error";
+    case TK_ERR_STATE: return "invalid state";
+    case TK_ERR_NOMEM: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+const char* tk_last_error(const tk_ctx* c) { return c ? c->err : "no context"; }
+
+}  // extern "C"

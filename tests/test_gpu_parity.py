@@ -1,0 +1,220 @@
+"""GPU parity: libtk (through the C ABI via the thin binding) against the CPU oracle, element by
+element on the same seeded inputs.  Bar (BASELINE.json north_star): thresholds, counts, index
+sets, values and residuals bit-exact; rank-ordered aggregates bit-exact."""
+import numpy as np
+import pytest
+
+import gradgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def tk():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests selected but no CUDA device is visible")
+    import paper_2010_10458_b200 as tk
+    return tk
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _f32bits(t):
+    return t.cpu().numpy().astype(np.float32).view(np.uint32)
+
+
+def _check_stats(st, ref):
+    s = ref.sel
+    assert st.mean == s.mean, (st.mean, s.mean)
+    assert st.max_bits == int(np.float32(s.u).view(np.uint32))
+    assert len(st.trials) == len(s.trials)
+    for it, (a, b) in enumerate(zip(st.trials, s.trials)):
+        assert a[0] == b[0] and a[1] == b[1] and a[2] == b[2] and a[3] == b[3], (it, a, b)
+    assert (st.k1, st.k2) == (s.k1, s.k2)
+    assert st.thres1_set == s.thres1_set and st.thres2_set == s.thres2_set
+    assert st.thres1 == s.thres1 and st.thres2 == s.thres2
+    assert (st.key1, st.key2) == (s.key1, s.key2)
+    assert st.len2 == s.len2 and st.rand == s.rand
+
+
+def _compress_case(tk, d, dist, k, N, *, ef=True, seed=0, step=0, rank=0, rand_mode="seeded", levels=0, cfg=1,
+                   r_scale=0.0):
+    g = gradgen.gradient(d, dist, cfg=cfg, rank=rank, step=step)
+    r = (gradgen.gradient(d, "G", cfg=cfg + 100, rank=rank, step=step) * np.float32(r_scale)).astype(np.float32)
+    ctx = tk.Context(d, k=k, n_iters=N, seed=seed, rand_mode=rand_mode, error_feedback=ef, levels_per_pass=levels)
+    ctx.set_step(step)
+    gd, rd = _dev(g), _dev(r)
+    idx, val = ctx.compress(gd, rd if ef else None)
+    torch.cuda.synchronize()
+    ref = oracle.compress(g, r if ef else None, k, N, seed=seed, step=step, rank=rank,
+                          rand_mode=oracle.RAND_FIRST if rand_mode == "first" else oracle.RAND_SEEDED,
+                          error_feedback=ef)
+    _check_stats(ctx.stats(), ref)
+    assert np.array_equal(_u32(idx), ref.sel.idx)
+    assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32))
+    if ef:
+        assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32))
+    else:
+        assert np.array_equal(_f32bits(gd), g.view(np.uint32))  # g never written
+    ctx.close()
+    return ref
+
+
+EDGE_D = [1, 2, 3, 4, 5, 127, 128, 129, 511, 4095, 4096, 4097, 8191, 12289, (1 << 20) + 3]
+
+
+@pytest.mark.parametrize("d", EDGE_D)
+def test_compress_edge_sizes(tk, d):
+    _compress_case(tk, d, "G", max(1, d // 100), 10, r_scale=0.1)
+
+
+@pytest.mark.parametrize("dist", gradgen.DISTS)
+@pytest.mark.parametrize("d,rho,N", [(1000, 0.01, 10), (65537, 0.001, 10), (300001, 0.001, 20), (100000, 0.01, 5)])
+def test_compress_distributions(tk, dist, d, rho, N):
+    _compress_case(tk, d, dist, oracle.k_from_density(d, rho), N, seed=3, step=1, r_scale=0.05)
+
+
+@pytest.mark.parametrize("levels", [1, 2, 3, 4])
+@pytest.mark.parametrize("N", [1, 2, 3, 7, 10, 13, 30, 52])
+def test_compress_levels_per_pass_invariance(tk, levels, N):
+    _compress_case(tk, 50003, "L", 50, N, levels=levels, seed=5)
+
+
+@pytest.mark.parametrize("k", [1, 2, 999, 10000])
+def test_compress_k_extremes(tk, k):
+    _compress_case(tk, 10000, "H", k, 10, seed=9)
+
+
+def test_compress_no_error_feedback_and_first_mode(tk):
+    _compress_case(tk, 1_000_000, "G", 1000, 10, ef=False)  # BASELINE config 1 (C1)
+    _compress_case(tk, 77777, "ties8", 77, 10, rand_mode="first")
+
+
+@pytest.mark.parametrize("case", ["E1_mstopk_bisection.json", "E2_thres2_unset.json", "E3_k1_zero_guard.json"])
+def test_compress_worked_examples(tk, golden, case):
+    gd = golden(case)
+    x = np.array(gd["x"], np.float32)
+    ctx = tk.Context(len(x), k=gd["k"], n_iters=gd["N"], rand_mode="first", error_feedback=False)
+    idx, val = ctx.compress(_dev(x))
+    st = ctx.stats()
+    assert [(t[0], t[1], t[3]) for t in st.trials] == [tuple(t) for t in gd["trials"]]
+    assert _u32(idx).tolist() == gd["idx"] and val.cpu().tolist() == gd["val"]
+
+
+def test_error_feedback_multi_step(tk):
+    d, k, N = 200003, 200, 10
+    ctx = tk.Context(d, k=k, n_iters=N, seed=77)
+    r_ref = np.zeros(d, np.float32)
+    rd = _dev(r_ref)
+    for step in range(4):
+        g = gradgen.gradient(d, "L", cfg=2, step=step)
+        idx, val = ctx.compress(_dev(g), rd)
+        ref = oracle.compress(g, r_ref, k, N, seed=77, step=step)
+        _check_stats(ctx.stats(), ref)
+        assert np.array_equal(_u32(idx), ref.sel.idx)
+        assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32))
+        assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32))
+        r_ref = ref.residual
+        ctx.set_step(step + 1)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8, 17])
+@pytest.mark.parametrize("d,rho", [(5000, 0.01), (1 << 20, 0.001), (1_000_003, 0.01), (4097, 0.5)])
+def test_decompress_rank_ordered(tk, P, d, rho):
+    k = oracle.k_from_density(d, rho)
+    gs = [gradgen.gradient(d, "G", cfg=20, rank=p) for p in range(P)]
+    res = oracle.flat_step(gs, [np.zeros(d, np.float32)] * P, rho, 10, seed=1)
+    ctx = tk.Context(d, k=k, n_iters=10)
+    out = ctx.decompress(_dev(res.gathered.view(np.int32)), nchunks=P)
+    assert np.array_equal(_f32bits(out), res.out.view(np.uint32))
+
+
+def test_decompress_overlapping_indices_rank_order(tk):
+    # every rank hits the same indices: the accumulation order decides the bits
+    d, P, k = 10000, 8, 500
+    rng = np.random.default_rng(4)
+    idx = np.sort(rng.choice(d, k, replace=False)).astype(np.uint32)
+    chunks = [oracle.pack(idx, (rng.standard_normal(k) * 10.0 ** rng.uniform(-8, 8, k)).astype(np.float32))
+              for _ in range(P)]
+    gathered = oracle.allgather(chunks)
+    want = oracle.decompress(gathered, P, k, d)
+    ctx = tk.Context(d, k=k, n_iters=10)
+    out = ctx.decompress(_dev(gathered.view(np.int32)), nchunks=P)
+    assert np.array_equal(_f32bits(out), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("d,rho,dist", [(1_000_000, 0.001, "G"), (3_000_017, 0.01, "L"), (4096, 1.0, "H")])
+def test_flat_step_single_rank(tk, d, rho, dist):
+    k = oracle.k_from_density(d, rho)
+    ctx = tk.Context(d, rho=rho, n_iters=10, seed=2)
+    r = np.zeros(d, np.float32)
+    rd = _dev(r)
+    for step in range(3):
+        g = gradgen.gradient(d, dist, cfg=30, step=step)
+        gat = torch.empty(2 * k, dtype=torch.int32, device="cuda")
+        out = ctx.step(_dev(g), rd, gathered=gat)
+        ref = oracle.flat_step([g], [r], rho, 10, seed=2, step=step)
+        assert np.array_equal(_u32(gat), ref.gathered)
+        assert np.array_equal(_f32bits(out), ref.out.view(np.uint32))
+        assert np.array_equal(_f32bits(rd), ref.per_rank[0].residual.view(np.uint32))
+        r = ref.per_rank[0].residual
+
+
+def test_step_host_matches_device_path(tk):
+    d, rho = 500_000, 0.001
+    ctx = tk.Context(d, rho=rho, n_iters=10, seed=8)
+    r = np.zeros(d, np.float32)
+    for step in range(2):
+        g = gradgen.gradient(d, "G", cfg=31, step=step)
+        gat = np.empty(2 * ctx.k, np.uint32)
+        out = np.empty(d, np.float32)
+        ctx.step_host(g, gat, out)
+        ref = oracle.flat_step([g], [r], rho, 10, seed=8, step=step)
+        assert np.array_equal(gat, ref.gathered)
+        assert np.array_equal(out.view(np.uint32), ref.out.view(np.uint32))
+        r = ref.per_rank[0].residual
+
+
+def test_nonfinite_is_reported(tk):
+    d = 10000
+    g = gradgen.gradient(d, "G", cfg=1)
+    g[1234] = np.inf
+    ctx = tk.Context(d, k=10, n_iters=10, error_feedback=False)
+    ctx.compress(_dev(g))
+    assert ctx.stats().nonfinite
+
+
+def test_rejects_cpu_and_wrong_dtype(tk):
+    ctx = tk.Context(1000, k=10, n_iters=10)
+    with pytest.raises(ValueError):
+        ctx.compress(torch.zeros(1000), torch.zeros(1000))
+    with pytest.raises(TypeError):
+        ctx.compress(torch.zeros(1000, dtype=torch.float64, device="cuda"), torch.zeros(1000, device="cuda"))
+
+
+@pytest.mark.parametrize("step", [0, 1])
+def test_compress_full_size_c2(tk, step):
+    """BASELINE config 2 at full size (d = 25.6M, rho = 1e-3, N = 10, error feedback), in the
+    launch configuration bench.py times; every field compared."""
+    d, rho, N = 25_600_000, 0.001, 10
+    k = oracle.k_from_density(d, rho)
+    r = (gradgen.gradient(d, "G", cfg=2, step=99) * np.float32(0.3 * step)).astype(np.float32)
+    g = gradgen.gradient(d, "G", cfg=2, step=step)
+    ctx = tk.Context(d, rho=rho, n_iters=N, seed=1234)
+    ctx.set_step(step)
+    rd = _dev(r)
+    idx, val = ctx.compress(_dev(g), rd)
+    ref = oracle.compress(g, r, k, N, seed=1234, step=step)
+    _check_stats(ctx.stats(), ref)
+    assert np.array_equal(_u32(idx), ref.sel.idx)
+    assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32))
+    assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32))
