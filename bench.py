@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the MSTopK + sparse-aggregation hot path (arXiv 2010.10458 CommLib) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W]                 # libtk (this repo)
+    python bench.py --impl reference [--gpus N --steps K --warmup W] # the CPU oracle (reference arm)
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+One step = one whole iteration of the hot path on every rank: error feedback, MSTopK (N = 10
+samplings), compaction into (index, value) pairs, the sparse All-Gather across the P ranks,
+rank-ordered decompression into the dense aggregate, residual write-back.
+Workload (BASELINE.json configs[1], C2): d = 25.6M fp32 gradient per rank, rho = 1e-3
+(k = 25 600), N = 10, error feedback on; P = N GPUs, flat NaiveAG (weak scaling: every rank
+brings its own d-vector).  Metric: elements/s = P*d / (max-over-ranks device time per step).
+
+Rank 0 prints ONE JSON line.  See DESIGN.md §Measurement for the roofline accounting.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import gradgen  # noqa: E402  (seeded inputs only; no method arithmetic)
+
+METRIC = "MSTopK+aggregation elements/s"
+UNIT = "elements/s"
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="tk", choices=["tk", "reference"])
+    ap.add_argument("--d", type=int, default=25_600_000)
+    ap.add_argument("--rho", type=float, default=0.001)
+    ap.add_argument("--n-iters", type=int, default=10)
+    ap.add_argument("--dist", default="G")
+    ap.add_argument("--group-size", type=int, default=1, help="HiTopKComm n (1 = flat NaiveAG)")
+    ap.add_argument("--step4", default="dense", choices=["dense", "sparse"])
+    ap.add_argument("--levels", type=int, default=0, help="bisection levels per count pass (0 = default)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="short run for ncu: no soak, no e2e, no cpu baseline")
+    return ap.parse_args()
+
+
+def workload_name(a, P):
+    if a.group_size > 1:
+        return f"C4 HiTopKComm {P // a.group_size}x{a.group_size} d={a.d} rho={a.rho} N={a.n_iters}"
+    tag = "C2" if a.d == 25_600_000 else ("C3" if a.d == 110_000_000 else "custom")
+    return f"{tag} flat sparse allgather d={a.d} rho={a.rho} N={a.n_iters} EF P={P}"
+
+
+def k_of(d, rho):
+    import math
+    return max(1, int(math.floor(float(rho) * float(d))))
+
+
+def measured_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        self.path = f"/tmp/tk_clocks_{os.getpid()}.csv"
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ dist
+def dist_setup(a):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.gpus != ws:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={ws}: launch N>1 with torchrun")
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if torch.cuda.is_available() and a.impl == "tk":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------------------ CPU oracle
+def time_oracle_step(d, rho, N, P, n, seed=1, dist="G"):
+    """One full simulated step of the oracle (all P ranks in one process); returns seconds."""
+    import oracle
+    gs = [gradgen.gradient(d, dist, cfg=2, rank=p, step=0) for p in range(P)]
+    t0 = time.perf_counter()
+    if n == 1:
+        rs = [np.zeros(d, np.float32) for _ in range(P)]
+        oracle.flat_step(gs, rs, rho, N, seed=seed)
+    else:
+        rs = [np.zeros(d // n, np.float32) for _ in range(P)]
+        oracle.hitopk_step(gs, rs, P // n, n, rho, N, seed=seed)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(a, P, budget_s=15.0):
+    d_s = a.d
+    t = time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist)
+    reps, total = 1, t
+    while total < budget_s and reps < 30:
+        total += time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist)
+        reps += 1
+    return {"value": d_s * reps / total, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{reps} full single-rank oracle steps (numpy, 1 thread) at d={d_s}, rho={a.rho}, N={a.n_iters}, "
+                      f"EF; {total:.1f} s of CPU work; host has {host_cores()} cores"}
+
+
+def run_reference(a, ws, rank):
+    if rank != 0:
+        return
+    P = ws
+    n = a.group_size
+    d_s = max(n * 4096, (min(a.d, 25_600_000 // P) // n) * n)  # bounded sample of the workload per step
+    for _ in range(a.warmup):
+        time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist)
+    ts = [time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist) for _ in range(a.steps)]
+    t = sum(ts) / len(ts)
+    val = P * d_s / t
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(a, P), "d": a.d, "rho": a.rho, "n_iters": a.n_iters, "P": P,
+                       "group_size": n, "dist": a.dist, "sample_d_per_rank": d_s},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"each step: the whole {P}-rank step simulated in one process on d={d_s} per rank "
+                                       f"(bounded sample of d={a.d}); numpy, 1 thread; host has {host_cores()} cores"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ libtk arm
+def stage_bytes(name, L, d, k, P, ef, chunks):
+    """Algorithmic HBM bytes of ONE launch of a stage."""
+    if name == "k_ef_stats":
+        return (12 if ef else 4) * L
+    if name.startswith("k_count"):
+        return 4 * L
+    if name == "k_select":
+        return 4 * L + 8 * k + (4 * k if ef else 0)
+    if name == "k_decompress":
+        return 4 * d + 8 * chunks * k
+    if name == "k_tile_ranges":
+        return 4 * chunks * k
+    return None
+
+
+def main():
+    a = parse()
+    ws, rank, local = dist_setup(a)
+    if a.impl == "reference":
+        run_reference(a, ws, rank)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    import torch
+    import paper_2010_10458_b200 as tk
+    torch.cuda.set_device(local)
+    P = ws
+    n = a.group_size
+    uid = tk.broadcast_unique_id() if P > 1 else None
+    stream = torch.cuda.Stream()
+    ctx = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, nranks=P, rank=rank, group_size=n, seed=2010_10458,
+                     step4=a.step4, levels_per_pass=a.levels, uid=uid, stream=stream, device=local)
+    L, k = ctx.seg_len, ctx.k
+    # inputs: a fresh seeded N(0,1) gradient for every warm-up / timed / profiled step, generated on
+    # the device before any timing (pool capped at ~16 GB per rank; reused cyclically beyond that)
+    need = a.warmup + 2 * a.steps
+    nbuf = max(2, min(need, int(16e9 // (4 * a.d))))
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(201010458 + 1000 * rank)
+    with torch.cuda.stream(stream):
+        if a.dist == "G":
+            gs = [torch.randn(a.d, generator=gen, device="cuda", dtype=torch.float32) for _ in range(nbuf)]
+        else:
+            gs = [torch.from_numpy(gradgen.gradient(a.d, a.dist, cfg=2, rank=rank, step=s)).cuda() for s in range(nbuf)]
+        r = torch.zeros(L, dtype=torch.float32, device="cuda")
+        r_soak = torch.zeros(L, dtype=torch.float32, device="cuda")
+        out = torch.empty(a.d, dtype=torch.float32, device="cuda")
+    stream.synchronize()
+    cursor = [0]
+
+    def run(steps, rr=None):
+        rr = r if rr is None else rr
+        for _ in range(steps):
+            ctx.step(gs[cursor[0] % nbuf], rr, out)
+            cursor[0] += 1
+
+    sampler = None if a.ncu else ClockSampler(local)
+    if not a.ncu:
+        # keep the GPU under this load ~1 s (on a scratch residual) so the clock samples describe
+        # the timed region's regime
+        t_end = time.time() + 1.0
+        with torch.cuda.stream(stream):
+            while time.time() < t_end:
+                run(20, r_soak)
+                stream.synchronize()
+    # the measured error-feedback run starts from r = 0 at step 0 with fresh gradients
+    cursor[0] = 0
+    ctx.set_step(0)
+    with torch.cuda.stream(stream):
+        r.zero_()
+        run(a.warmup)
+    stream.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    l0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        run(a.steps)
+        e1.record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = sampler.stop() if sampler else None
+    launches = ctx.launches - l0
+    t_step = max_over_ranks(e0.elapsed_time(e1) / a.steps, ws)  # ms, max over ranks
+    gpu_launches = int(sum_over_ranks(launches, ws))
+    value = P * a.d / (t_step * 1e-3)
+
+    # per-stage breakdown over K more steps with stage events (same stream, same buffers)
+    ctx.profile_begin(a.steps)
+    with torch.cuda.stream(stream):
+        run(a.steps)
+    prof = ctx.profile_end()
+    chunks = P if n == 1 else P // n
+    stages = {}
+    for name, (ms, cnt) in prof.items():
+        stages[name] = {"ms_per_launch": ms / cnt, "launches_per_step": cnt / a.steps,
+                        "share": ms / a.steps / t_step if t_step > 0 else None}
+    compute = {kname: v for kname, v in stages.items() if kname.startswith("k_")}
+    dom = max(compute, key=lambda kn: compute[kn]["ms_per_launch"] * compute[kn]["launches_per_step"])
+    peak, peak_src = measured_hbm()
+    bytes_launch = stage_bytes(dom, L, a.d, k, P, True, chunks)
+    achieved = bytes_launch / (stages[dom]["ms_per_launch"] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tr = json.load(open(tp))
+            key = f"{dom}@d={L}"
+            traffic = tr.get(key)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_launch,
+                "ms_per_launch": stages[dom]["ms_per_launch"],
+                "note": "achieved = algorithmic bytes per launch / mean CUDA-event duration of that launch inside "
+                        "the profiled steps; count passes at d=25.6M re-read a 102 MB vector that is L2-resident "
+                        "(126 MB L2) within a step"}
+
+    # end-to-end through the public host-buffer API: pinned H2D of g + D2H of the gathered pairs
+    e2e = None
+    if not a.no_e2e and not a.ncu:
+        ctx_h = ctx
+        hg = [torch.from_numpy(gradgen.gradient(a.d, a.dist, cfg=2, rank=rank, step=s)).pin_memory() for s in range(2)]
+        gat_h = torch.empty(chunks * 2 * k, dtype=torch.int32).pin_memory()
+        for i in range(3):
+            ctx_h.step_host(hg[i % 2], gat_h)
+        barrier(ws)
+        ks = max(5, min(a.steps, 50))
+        t0 = time.perf_counter()
+        for i in range(ks):
+            ctx_h.step_host(hg[i % 2], gat_h)
+        t_e2e = max_over_ranks((time.perf_counter() - t0) / ks, ws)
+        e2e = {"value": P * a.d / t_e2e, "unit": UNIT, "ms_per_step": t_e2e * 1e3,
+               "h2d_bytes_per_step": 4 * a.d, "d2h_bytes_per_step": 4 * chunks * 2 * k,
+               "api": "tk_step_host (pinned host gradient in, gathered (index, value) pairs out; residual device-resident)"}
+
+    cpu = None
+    if rank == 0 and P == 1 and not a.no_cpu_baseline and not a.ncu:
+        cpu = cpu_baseline(a, P)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": P, "steps": a.steps, "warmup": a.warmup,
+                "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": workload_name(a, P), "d": a.d, "rho": a.rho, "k": k, "n_iters": a.n_iters,
+                           "P": P, "group_size": n, "step4": a.step4 if n > 1 else None, "dist": a.dist,
+                           "levels_per_pass": a.levels or 4, "input_buffers": nbuf,
+                           "inputs": "fresh seeded N(0,1) gradient per step (torch CUDA generator, pre-generated in "
+                                     "HBM); residual carried from r=0 at step 0; timed steps W..W+K-1",
+                           "l2": "inputs larger than L2: each step reads a fresh g (4d B) and touches r and out: "
+                                 f"{12 * a.d / 1e6:.0f} MB per rank per step vs 126 MB L2; no explicit flush"},
+                "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "stages": stages}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

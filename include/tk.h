@@ -89,6 +89,8 @@ typedef struct tk_stats {
   uint64_t rand_start;     /* rand (l.27)                                                      */
   uint64_t step;           /* step counter used for this compression's RNG draw               */
   uint32_t nonfinite;      /* 1 if a NaN/Inf was seen (sticky)                                 */
+  uint32_t compacted;      /* 1 if passes 2.. and the selection ran on the entries compacted by
+                              the first count pass (an exact shortcut)          */
 } tk_stats;
 
 /* k = max(1, floor(rho * d)) in fp64 (Q13).  Host-only, pure.  0 on invalid input. */
@@ -147,6 +149,20 @@ tk_status tk_query(const tk_ctx* ctx, uint64_t* k, uint64_t* seg_len, uint32_t* 
 
 /* Number of kernel launches libtk enqueued on the context stream since init (evidence counter). */
 uint64_t tk_launch_count(const tk_ctx* ctx);
+
+/* Stage profiling with CUDA events on the context stream.  Between tk_profile_begin and
+ * tk_profile_end every tk_step records an event at each stage boundary (capacity max_steps
+ * steps).  tk_profile_end synchronises and returns, per stage, the summed device time in ms and
+ * the number of launches (ms / launches = mean duration of one launch of that stage). */
+enum {
+  TK_STAGE_NONE = 0, TK_STAGE_EF_STATS = 1, TK_STAGE_FINALIZE = 2, TK_STAGE_COUNT1 = 3, TK_STAGE_COUNT3 = 4,
+  TK_STAGE_COUNT7 = 5, TK_STAGE_COUNT15 = 6, TK_STAGE_SCAN = 7, TK_STAGE_SELECT = 8, TK_STAGE_ALLGATHER = 9,
+  TK_STAGE_TILE_RANGES = 10, TK_STAGE_DECOMPRESS = 11, TK_STAGE_REDUCE_SCATTER = 12,
+  TK_STAGE_STEP4_ALLGATHER = 13, TK_NSTAGES = 16
+};
+tk_status tk_profile_begin(tk_ctx* ctx, uint32_t max_steps);
+tk_status tk_profile_end(tk_ctx* ctx, double ms[TK_NSTAGES], uint32_t launches[TK_NSTAGES]);
+const char* tk_stage_name(uint32_t stage);
 
 tk_status tk_destroy(tk_ctx* ctx);
 const char* tk_status_string(tk_status s);

@@ -50,18 +50,20 @@ class _Stats(ctypes.Structure):
                 ("key1", ctypes.c_uint32), ("key2", ctypes.c_uint32),
                 ("thres1_set", ctypes.c_uint32), ("thres2_set", ctypes.c_uint32),
                 ("len2", ctypes.c_uint64), ("rand_start", ctypes.c_uint64), ("step", ctypes.c_uint64),
-                ("nonfinite", ctypes.c_uint32)]
+                ("nonfinite", ctypes.c_uint32), ("compacted", ctypes.c_uint32)]
 
 
 # Every symbol include/tk.h declares (checked by tests/test_abi.py).
 EXPORTS = ["tk_k", "tk_get_unique_id", "tk_init", "tk_compress", "tk_sparse_allgather", "tk_decompress",
            "tk_step", "tk_step_host", "tk_get_stats", "tk_set_step", "tk_query", "tk_launch_count",
-           "tk_destroy", "tk_status_string", "tk_last_error"]
+           "tk_destroy", "tk_status_string", "tk_last_error", "tk_profile_begin", "tk_profile_end",
+           "tk_stage_name"]
+NSTAGES = 16
 
 
 def _load():
     if not os.path.exists(_LIB_PATH):
-        raise ImportError(f"libtk.so not built at {_LIB_PATH}: run `python -m paper_2010_10458_b200.build` "
+        raise ImportError(f"libtk.so not built at {_LIB_PATH}: run `python paper_2010_10458_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(_LIB_PATH)
     P, U32, U64, I32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
@@ -82,6 +84,9 @@ def _load():
         "tk_destroy": (I32, [P]),
         "tk_status_string": (ctypes.c_char_p, [I32]),
         "tk_last_error": (ctypes.c_char_p, [P]),
+        "tk_profile_begin": (I32, [P, U32]),
+        "tk_profile_end": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(U32)]),
+        "tk_stage_name": (ctypes.c_char_p, [U32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -161,6 +166,7 @@ class Stats:
     rand: int
     step: int
     nonfinite: bool
+    compacted: bool
 
 
 class Context:
@@ -257,10 +263,21 @@ class Context:
         trials = [(s.ratio[i], s.thres[i], s.key[i], s.nnz[i]) for i in range(s.n_trials)]
         return Stats(mean=s.mean, max_bits=s.max_bits, trials=trials, k=s.k, k1=s.k1, k2=s.k2, thres1=s.thres1,
                      thres2=s.thres2, thres1_set=bool(s.thres1_set), thres2_set=bool(s.thres2_set), key1=s.key1,
-                     key2=s.key2, len2=s.len2, rand=s.rand_start, step=s.step, nonfinite=bool(s.nonfinite))
+                     key2=s.key2, len2=s.len2, rand=s.rand_start, step=s.step, nonfinite=bool(s.nonfinite),
+                     compacted=bool(s.compacted))
 
     def set_step(self, step: int):
         self._check(_lib.tk_set_step(self._ctx, int(step)))
+
+    def profile_begin(self, max_steps: int):
+        self._check(_lib.tk_profile_begin(self._ctx, int(max_steps)))
+
+    def profile_end(self) -> dict:
+        """{stage name: (total ms, launches)} over the steps since profile_begin."""
+        ms = (ctypes.c_double * NSTAGES)()
+        ln = (ctypes.c_uint32 * NSTAGES)()
+        self._check(_lib.tk_profile_end(self._ctx, ms, ln))
+        return {_lib.tk_stage_name(i).decode(): (ms[i], ln[i]) for i in range(1, NSTAGES) if ln[i] > 0}
 
     @property
     def launches(self) -> int:

@@ -1,7 +1,7 @@
 """Build libtk.so in-tree for sm_100a with nvcc (no JIT cache: the .so travels with the repo).
 
-    python -m paper_2010_10458_b200.build            # release build
-    python -m paper_2010_10458_b200.build --verbose  # also print ptxas register/spill report
+    python paper_2010_10458_b200/build.py            # release build (never imports the package)
+    python paper_2010_10458_b200/build.py --verbose  # also print ptxas register/spill report
 """
 from __future__ import annotations
 

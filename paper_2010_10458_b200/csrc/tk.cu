@@ -28,21 +28,25 @@ struct tk_ctx {
   uint32_t P = 1, m = 1, n = 1, rank = 0;
   uint32_t row_pos = 0, col_pos = 0;  // j = rank % n (position in the node), i = rank / n (node)
   uint64_t d = 0, L = 0, k = 0;       // L = d / n (segment length); k = k (flat) or k~ (HiTopK)
-  uint32_t ntiles = 0;                // tiles of the vector MSTopK runs on (length L)
-  uint32_t ntiles_d = 0;              // tiles of d
-  uint32_t levels = 3, npass = 0;
+  uint32_t sms = 148;
+  uint32_t grid_stats = 0;            // K1 CTAs
+  uint32_t grid_slab = 0;             // K2/K4 CTAs (their warps partition [0, L) into slabs)
+  uint32_t W = 0;                     // warp slabs
+  uint64_t S = 0;                     // slab length
+  uint32_t occ_dec = 1;               // resident decompression CTAs per SM
+  uint32_t levels = 4, npass = 0;
   int lev_sched[NMAX];
-  double* tile_sum = nullptr;
-  uint32_t* tile_max = nullptr;
-  uint16_t* tile_counts = nullptr;
-  uint32_t* pre1 = nullptr;
+  uint32_t units_per_warp = 1;        // K1: aligned power-of-two run of 512-element units per warp
+  double* cta_sum = nullptr;          // K1 per-CTA partial sums / maxima
+  uint32_t* cta_max = nullptr;
+  uint32_t* wcnt = nullptr;           // per-warp-slab counts [npass*TMAX][W]
+  uint32_t* pre1 = nullptr;           // per-slab exclusive prefix of class-1 / class-2 counts
   uint32_t* pre2 = nullptr;
+  Compact cp;                         // compacted entries of the first count pass
   Ctrl* ctrl = nullptr;
   uint32_t* send = nullptr;      // [2k]
   uint32_t* recv = nullptr;      // flat: [P][2k]; HiTopK: [m][2k~]
   uint32_t* recv_row = nullptr;  // HiTopK sparse step 4: [n][m][2k~]
-  uint32_t* starts = nullptr;    // [max chunks][ntiles_d + 1]
-  uint32_t max_chunks = 1;
   float* seg = nullptr;          // HiTopK step-1 output [L]
   float* h_g = nullptr;          // tk_step_host device staging
   float* h_r = nullptr;
@@ -51,6 +55,12 @@ struct tk_ctx {
   uint64_t step = 0;
   uint64_t launches = 0;
   uint32_t nonfinite_sticky = 0;
+  // stage profiling (tk_profile_begin / tk_profile_end): events at stage boundaries
+  cudaEvent_t* prof_ev = nullptr;
+  uint8_t* prof_kind = nullptr;
+  uint32_t prof_cap = 0, prof_n = 0;
+  bool prof_on = false;
+  uint32_t prof_launch[TK_NSTAGES] = {0};
   char err[512] = {0};
 };
 
@@ -93,23 +103,34 @@ tk_status check_launch(tk_ctx* c, const char* what) {
   return TK_OK;
 }
 
+// Record a stage boundary: the interval since the previous mark is attributed to `kind`.
+void mark(tk_ctx* c, int kind) {
+  if (!c->prof_on || c->prof_n >= c->prof_cap) return;
+  cudaEventRecord(c->prof_ev[c->prof_n], c->stream);
+  c->prof_kind[c->prof_n] = (uint8_t)kind;
+  c->prof_n++;
+  if (kind > 0 && kind < TK_NSTAGES) c->prof_launch[kind]++;
+}
+
 SearchParams search_params(const tk_ctx* c) {
   SearchParams sp;
   sp.n = c->L;
   sp.k = c->k;
-  sp.ntiles = c->ntiles;
-  sp.n_iters = c->cfg.n_iters;
-  sp.levels = c->levels;
+  sp.W = c->W;
+  sp.S = c->S;
   sp.rank = c->rank;
-  sp.seed = c->cfg.seed;
   sp.rand_mode = c->cfg.rand_mode;
+  sp.seed = c->cfg.seed;
   return sp;
 }
 
-template <int T>
-tk_status launch_count(tk_ctx* c, const float* acc, const SearchParams& sp, int pass, int lev, int next_lev) {
-  k_count<T><<<c->ntiles, THREADS, 0, c->stream>>>(acc, c->ctrl, sp, c->tile_counts, pass, lev, next_lev);
-  return check_launch(c, "k_count");
+template <int LEV, bool FIRST>
+tk_status launch_count(tk_ctx* c, const float* acc, const SearchParams& sp, int pass, int next_lev) {
+  k_count<LEV, FIRST><<<c->grid_slab, THREADS, 0, c->stream>>>(acc, c->ctrl, sp, c->wcnt, c->pre1, c->pre2, c->cp,
+                                                                pass, next_lev);
+  tk_status s = check_launch(c, "k_count");
+  mark(c, LEV == 1 ? TK_STAGE_COUNT1 : LEV == 2 ? TK_STAGE_COUNT3 : LEV == 3 ? TK_STAGE_COUNT7 : TK_STAGE_COUNT15);
+  return s;
 }
 
 // MSTopK on a vector of length L (= c->L) with error feedback: g (+ r) -> idx/val.
@@ -117,43 +138,46 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   const bool ef = c->cfg.error_feedback != 0;
   const SearchParams sp = search_params(c);
   if (ef) {
-    k_ef_stats<true><<<c->ntiles, THREADS, 0, c->stream>>>(g, r, c->L, c->tile_sum, c->tile_max);
+    k_ef_stats<true><<<c->grid_stats, THREADS, 0, c->stream>>>(g, r, sp, c->units_per_warp, c->cta_sum, c->cta_max,
+                                                               c->ctrl, c->step, c->lev_sched[0]);
   } else {
-    k_ef_stats<false><<<c->ntiles, THREADS, 0, c->stream>>>(g, nullptr, c->L, c->tile_sum, c->tile_max);
+    k_ef_stats<false><<<c->grid_stats, THREADS, 0, c->stream>>>(g, nullptr, sp, c->units_per_warp, c->cta_sum,
+                                                                c->cta_max, c->ctrl, c->step, c->lev_sched[0]);
   }
   TK_TRY(check_launch(c, "k_ef_stats"));
+  mark(c, TK_STAGE_EF_STATS);
   const float* acc = ef ? r : g;
-  k_finalize<<<1, FIN_THREADS, 0, c->stream>>>(c->tile_sum, c->tile_max, c->ctrl, sp, c->step, c->lev_sched[0]);
-  TK_TRY(check_launch(c, "k_finalize"));
   for (uint32_t p = 0; p < c->npass; ++p) {
-    const int lev = c->lev_sched[p];
     const int next = (p + 1 < c->npass) ? c->lev_sched[p + 1] : 0;
-    switch (lev) {
-      case 1: TK_TRY(launch_count<1>(c, acc, sp, (int)p, lev, next)); break;
-      case 2: TK_TRY(launch_count<3>(c, acc, sp, (int)p, lev, next)); break;
-      case 3: TK_TRY(launch_count<7>(c, acc, sp, (int)p, lev, next)); break;
-      default: TK_TRY(launch_count<15>(c, acc, sp, (int)p, lev, next)); break;
+    if (p == 0) {
+      if (c->lev_sched[0] == 1) TK_TRY((launch_count<1, true>(c, acc, sp, 0, next)));
+      else TK_TRY((launch_count<2, true>(c, acc, sp, 0, next)));
+      continue;
+    }
+    switch (c->lev_sched[p]) {
+      case 1: TK_TRY((launch_count<1, false>(c, acc, sp, (int)p, next))); break;
+      case 2: TK_TRY((launch_count<2, false>(c, acc, sp, (int)p, next))); break;
+      case 3: TK_TRY((launch_count<3, false>(c, acc, sp, (int)p, next))); break;
+      default: TK_TRY((launch_count<4, false>(c, acc, sp, (int)p, next))); break;
     }
   }
-  k_scan<<<1, SCAN_THREADS, 0, c->stream>>>(c->ctrl, sp, c->tile_counts, c->pre1, c->pre2);
-  TK_TRY(check_launch(c, "k_scan"));
-  k_select<<<c->ntiles, THREADS, 0, c->stream>>>(acc, c->ctrl, sp, c->pre1, c->pre2, idx, val, ef ? r : nullptr);
+  k_select<<<c->grid_slab, THREADS, 0, c->stream>>>(acc, c->ctrl, sp, c->wcnt, c->pre1, c->pre2, idx, val,
+                                                    ef ? r : nullptr, c->cp);
   TK_TRY(check_launch(c, "k_select"));
+  mark(c, TK_STAGE_SELECT);
   return TK_OK;
 }
 
 // Rank-ordered decompression of nchunks chunks of kk pairs into out[0, len).
 tk_status decompress_impl(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, uint64_t kk, uint64_t len,
-                          float* out, bool clear_starts) {
+                          float* out) {
   const uint32_t nt = (uint32_t)((len + TILE - 1) / TILE);
-  if (clear_starts)
-    TK_CUDA(c, cudaMemsetAsync(c->starts, 0, sizeof(uint32_t) * (size_t)nchunks * (nt + 1), c->stream));
-  const uint64_t tot = (uint64_t)nchunks * (kk + 1);
-  const uint32_t blocks = (uint32_t)std::min<uint64_t>((tot + 255) / 256, 148ull * 16);
-  k_tile_ranges<<<blocks, 256, 0, c->stream>>>(gathered, nchunks, kk, len, nt, c->starts);
-  TK_TRY(check_launch(c, "k_tile_ranges"));
-  k_decompress<<<nt, THREADS, 0, c->stream>>>(gathered, nchunks, kk, len, nt, c->starts, out);
+  const uint32_t max_cta = c->sms * c->occ_dec;
+  const uint32_t per = (nt + max_cta - 1) / max_cta;
+  const uint32_t grid = (nt + per - 1) / per;
+  k_decompress<<<grid, THREADS, sizeof(uint32_t) * nchunks, c->stream>>>(gathered, nchunks, kk, len, nt, per, out);
   TK_TRY(check_launch(c, "k_decompress"));
+  mark(c, TK_STAGE_DECOMPRESS);
   return TK_OK;
 }
 
@@ -165,11 +189,56 @@ tk_status dev_alloc(tk_ctx* c, T** p, size_t count) {
   return TK_OK;
 }
 
+// Grid sizes (persistent: #SMs x resident CTAs), the warp-slab partition shared by the count
+// and selection kernels, and the hierarchical pairwise-sum partial arrays.
+tk_status plan_launches(tk_ctx* c) {
+  int v = 0;
+  TK_CUDA(c, cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, c->device));
+  c->sms = (uint32_t)v;
+  int o1 = 0, o2 = 0, o3 = 0, o4 = 0, o5 = 0, o6 = 0, o7 = 0;
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_ef_stats<true>, THREADS, 0));
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_count<2, true>, THREADS, 0));
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_count<2, false>, THREADS, 0));
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_count<3, false>, THREADS, 0));
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o5, k_count<4, false>, THREADS, 0));
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o6, k_select, THREADS, 0));
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o7, k_decompress, THREADS, 64 * sizeof(uint32_t)));
+  const uint32_t occ_slab = (uint32_t)std::max(1, std::min({o2, o3, o4, o5, o6}));
+  c->occ_dec = (uint32_t)std::max(1, o7);
+  const uint64_t L = c->L;
+  // K1: each warp an aligned power-of-two run of 512-element units, grid <= resident CTAs
+  const uint64_t units = (L + ROUND - 1) / ROUND;
+  const uint64_t cap1 = (uint64_t)c->sms * std::max(1, o1);
+  uint64_t upw = 1;
+  while ((units + WARPS * upw - 1) / (WARPS * upw) > cap1) upw <<= 1;
+  c->units_per_warp = (uint32_t)upw;
+  c->grid_stats = (uint32_t)((units + WARPS * upw - 1) / (WARPS * upw));
+  // count / select: W warp slabs of S elements, S a multiple of ROUND
+  const uint64_t chunks = (L + ROUND - 1) / ROUND;
+  c->grid_slab = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sms * occ_slab,
+                                                                     (chunks + WARPS - 1) / WARPS));
+  c->W = c->grid_slab * WARPS;
+  c->S = ((L + c->W - 1) / c->W + ROUND - 1) / ROUND * ROUND;  // whole rounds: no ragged slab ends
+  TK_TRY(dev_alloc(c, &c->cta_sum, c->grid_stats));
+  TK_TRY(dev_alloc(c, &c->cta_max, c->grid_stats));
+  // compacted entries: capacity S/4 per warp slab (the fallback path covers an overflow)
+  c->cp.C = (uint32_t)std::max<uint64_t>(4, (c->S / 4 + 3) / 4 * 4);
+  TK_TRY(dev_alloc(c, &c->cp.idx, (size_t)c->W * c->cp.C));
+  TK_TRY(dev_alloc(c, &c->cp.bits, (size_t)c->W * c->cp.C));
+  TK_TRY(dev_alloc(c, &c->cp.cnt, c->W));
+  return TK_OK;
+}
+
 void free_all(tk_ctx* c) {
-  void* ptrs[] = {c->tile_sum, c->tile_max, c->tile_counts, c->pre1, c->pre2, c->ctrl, c->send, c->recv,
-                  c->recv_row, c->starts, c->seg, c->h_g, c->h_r, c->h_out};
+  void* ptrs[] = {c->cp.idx, c->cp.bits, c->cp.cnt, c->cta_sum, c->cta_max, c->wcnt, c->pre1, c->pre2, c->ctrl, c->send, c->recv,
+                  c->recv_row, c->seg, c->h_g, c->h_r, c->h_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (c->prof_ev) {
+    for (uint32_t i = 0; i < c->prof_cap; ++i) cudaEventDestroy(c->prof_ev[i]);
+    delete[] c->prof_ev;
+    delete[] c->prof_kind;
+  }
   if (c->row) ncclCommDestroy(c->row);
   if (c->col) ncclCommDestroy(c->col);
   if (c->world) ncclCommDestroy(c->world);
@@ -227,13 +296,19 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   c->L = L;
   c->k = kk;
   c->stream = reinterpret_cast<cudaStream_t>(stream);
-  c->ntiles = (uint32_t)((L + TILE - 1) / TILE);
-  c->ntiles_d = (uint32_t)((k.d + TILE - 1) / TILE);
-  c->levels = k.levels_per_pass == 0 ? 3 : k.levels_per_pass;
-  for (uint32_t done = 0; done < k.n_iters;) {
-    const uint32_t lev = std::min(c->levels, k.n_iters - done);
-    c->lev_sched[c->npass++] = (int)lev;
-    done += lev;
+  c->levels = k.levels_per_pass == 0 ? 4 : k.levels_per_pass;
+  // pass schedule: the first pass resolves min(2, levels) levels (its candidates spread over the
+  // whole [a-bar, u] range, where the full bucket search runs on every element); the remaining
+  // levels go in balanced passes of <= levels (their candidates bracket a narrow band, so most
+  // elements skip the search).  The result bits do not depend on the schedule.
+  {
+    const uint32_t first = std::min<uint32_t>(std::min<uint32_t>(2u, c->levels), k.n_iters);
+    c->lev_sched[c->npass++] = (int)first;
+    const uint32_t rest = k.n_iters - first;
+    if (rest > 0) {
+      const uint32_t np = (rest + c->levels - 1) / c->levels;
+      for (uint32_t p = 0; p < np; ++p) c->lev_sched[c->npass++] = (int)(rest / np + (p < rest % np ? 1 : 0));
+    }
   }
   auto bail = [&](tk_status s) {
     free_all(c);
@@ -246,17 +321,14 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   }
   cudaGetDevice(&c->device);
   tk_status s;
-  if ((s = dev_alloc(c, &c->tile_sum, c->ntiles)) != TK_OK) return bail(s);
-  if ((s = dev_alloc(c, &c->tile_max, c->ntiles)) != TK_OK) return bail(s);
-  if ((s = dev_alloc(c, &c->tile_counts, (size_t)c->npass * TMAX * c->ntiles)) != TK_OK) return bail(s);
-  if ((s = dev_alloc(c, &c->pre1, c->ntiles)) != TK_OK) return bail(s);
-  if ((s = dev_alloc(c, &c->pre2, c->ntiles)) != TK_OK) return bail(s);
+  if ((s = plan_launches(c)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->wcnt, (size_t)c->npass * TMAX * c->W)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->pre1, c->W)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->pre2, c->W)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->ctrl, 1)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->send, 2 * kk)) != TK_OK) return bail(s);
   const uint32_t chunks_recv = (n == 1) ? c->P : c->m;
   if ((s = dev_alloc(c, &c->recv, (size_t)chunks_recv * 2 * kk)) != TK_OK) return bail(s);
-  c->max_chunks = std::max<uint32_t>(c->P, 1);
-  if ((s = dev_alloc(c, &c->starts, (size_t)c->max_chunks * (c->ntiles_d + 1))) != TK_OK) return bail(s);
   if (n > 1) {
     if ((s = dev_alloc(c, &c->seg, L)) != TK_OK) return bail(s);
     if (k.step4 == TK_STEP4_SPARSE)
@@ -317,15 +389,8 @@ tk_status tk_decompress(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, f
   if (!gathered || !out) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
   if (!aligned16(out)) return fail(c, TK_ERR_INVALID_ARG, "out must be 16-byte aligned");
   if (nchunks < 1 || nchunks > 4096) return fail(c, TK_ERR_INVALID_ARG, "nchunks must lie in [1, 4096]");
-  if (nchunks > c->max_chunks) {  // grow the range table (synchronises the stream)
-    TK_CUDA(c, cudaStreamSynchronize(c->stream));
-    TK_CUDA(c, cudaFree(c->starts));
-    c->starts = nullptr;
-    TK_TRY(dev_alloc(c, &c->starts, (size_t)nchunks * (c->ntiles_d + 1)));
-    c->max_chunks = nchunks;
-  }
   const uint64_t len = (c->n == 1) ? c->d : c->L;
-  return decompress_impl(c, gathered, nchunks, c->k, len, out, true);
+  return decompress_impl(c, gathered, nchunks, c->k, len, out);
 }
 
 tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gathered) {
@@ -337,6 +402,7 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
     return fail(c, TK_ERR_INVALID_ARG, "g, r and out must not alias");
   uint32_t* send = c->send;
   const size_t kb = sizeof(uint32_t) * c->k;
+  mark(c, TK_STAGE_NONE);
   if (c->n == 1) {
     // flat NaiveAG: compress -> one packed all-gather -> rank-ordered decompress
     TK_TRY(compress_impl(c, g, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k)));
@@ -346,10 +412,12 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
     } else {
       TK_CUDA(c, cudaMemcpyAsync(gat, send, 2 * kb, cudaMemcpyDeviceToDevice, c->stream));
     }
-    TK_TRY(decompress_impl(c, gat, c->P, c->k, c->d, out, false));
+    mark(c, TK_STAGE_ALLGATHER);
+    TK_TRY(decompress_impl(c, gat, c->P, c->k, c->d, out));
   } else {
     // HiTopKComm (Alg. 2).  Step 1: intra-node reduce-scatter of g (Eq. 4).
     TK_NCCL(c, ncclReduceScatter(g, c->seg, c->L, ncclFloat32, ncclSum, c->row, c->stream));
+    mark(c, TK_STAGE_REDUCE_SCATTER);
     // Step 2: MSTopK on the segment with k~ (Eq. 5), error feedback on the segment residual.
     TK_TRY(compress_impl(c, c->seg, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k)));
     // Step 3: inter-node all-gather among the m GPUs at the same position j (Eq. 6) ...
@@ -359,19 +427,22 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
     } else {
       TK_CUDA(c, cudaMemcpyAsync(gat, send, 2 * kb, cudaMemcpyDeviceToDevice, c->stream));
     }
+    mark(c, TK_STAGE_ALLGATHER);
     float* my_seg = out + (size_t)c->row_pos * c->L;
     if (c->cfg.step4 == TK_STEP4_DENSE) {
       // ... accumulated in group order into this GPU's segment, then step 4: dense intra-node
       // all-gather of the segments (Alg. 2 l.21-23), in place.
-      TK_TRY(decompress_impl(c, gat, c->m, c->k, c->L, my_seg, false));
+      TK_TRY(decompress_impl(c, gat, c->m, c->k, c->L, my_seg));
       TK_NCCL(c, ncclAllGather(my_seg, out, c->L, ncclFloat32, c->row, c->stream));
+      mark(c, TK_STAGE_STEP4_ALLGATHER);
     } else {
       // step 4 sparse (Eq. 10): all-gather the m*k~ gathered pairs of every segment, then every
       // GPU accumulates all segments itself (same per-element order -> identical bits).
       TK_NCCL(c, ncclAllGather(gat, c->recv_row, (size_t)c->m * 2 * c->k, ncclUint32, c->row, c->stream));
+      mark(c, TK_STAGE_STEP4_ALLGATHER);
       for (uint32_t j = 0; j < c->n; ++j)
         TK_TRY(decompress_impl(c, c->recv_row + (size_t)j * c->m * 2 * c->k, c->m, c->k, c->L,
-                               out + (size_t)j * c->L, false));
+                               out + (size_t)j * c->L));
     }
   }
   c->step++;
@@ -429,6 +500,7 @@ tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
   st->step = h.step;
   c->nonfinite_sticky |= h.nonfinite;
   st->nonfinite = c->nonfinite_sticky;
+  st->compacted = h.cap_ok;
   if (c->nonfinite_sticky) return fail(c, TK_ERR_NONFINITE, "non-finite value in acc (precondition, Q24)");
   return TK_OK;
 }
@@ -450,6 +522,52 @@ tk_status tk_query(const tk_ctx* c, uint64_t* k, uint64_t* seg_len, uint32_t* nr
 }
 
 uint64_t tk_launch_count(const tk_ctx* c) { return c ? c->launches : 0; }
+
+tk_status tk_profile_begin(tk_ctx* c, uint32_t max_steps) {
+  if (!c || max_steps == 0) return TK_ERR_INVALID_ARG;
+  const uint32_t need = max_steps * 32u;
+  if (need > c->prof_cap) {
+    if (c->prof_ev) {
+      TK_CUDA(c, cudaStreamSynchronize(c->stream));
+      for (uint32_t i = 0; i < c->prof_cap; ++i) cudaEventDestroy(c->prof_ev[i]);
+      delete[] c->prof_ev;
+      delete[] c->prof_kind;
+    }
+    c->prof_ev = new (std::nothrow) cudaEvent_t[need];
+    c->prof_kind = new (std::nothrow) uint8_t[need];
+    if (!c->prof_ev || !c->prof_kind) return TK_ERR_NOMEM;
+    for (uint32_t i = 0; i < need; ++i) TK_CUDA(c, cudaEventCreate(&c->prof_ev[i]));
+    c->prof_cap = need;
+  }
+  c->prof_n = 0;
+  memset(c->prof_launch, 0, sizeof(c->prof_launch));
+  c->prof_on = true;
+  return TK_OK;
+}
+
+tk_status tk_profile_end(tk_ctx* c, double ms[TK_NSTAGES], uint32_t launches[TK_NSTAGES]) {
+  if (!c || !ms) return TK_ERR_INVALID_ARG;
+  c->prof_on = false;
+  for (int i = 0; i < TK_NSTAGES; ++i) ms[i] = 0.0;
+  TK_CUDA(c, cudaStreamSynchronize(c->stream));
+  for (uint32_t i = 1; i < c->prof_n; ++i) {
+    const int kind = c->prof_kind[i];
+    if (kind == TK_STAGE_NONE) continue;  // a step's opening mark: the gap to it is not a stage
+    float t = 0.f;
+    TK_CUDA(c, cudaEventElapsedTime(&t, c->prof_ev[i - 1], c->prof_ev[i]));
+    ms[kind] += (double)t;
+  }
+  if (launches) memcpy(launches, c->prof_launch, sizeof(c->prof_launch));
+  return TK_OK;
+}
+
+const char* tk_stage_name(uint32_t stage) {
+  static const char* names[TK_NSTAGES] = {"none", "k_ef_stats", "k_finalize", "k_count<1>", "k_count<3>",
+                                          "k_count<7>", "k_count<15>", "k_scan", "k_select", "allgather",
+                                          "k_tile_ranges", "k_decompress", "reduce_scatter", "step4_allgather",
+                                          "reserved14", "reserved15"};
+  return stage < TK_NSTAGES ? names[stage] : "invalid";
+}
 
 tk_status tk_destroy(tk_ctx* c) {
   if (!c) return TK_ERR_INVALID_ARG;

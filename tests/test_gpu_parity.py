@@ -58,7 +58,8 @@ def _compress_case(tk, d, dist, k, N, *, ef=True, seed=0, step=0, rank=0, rand_m
     ref = oracle.compress(g, r if ef else None, k, N, seed=seed, step=step, rank=rank,
                           rand_mode=oracle.RAND_FIRST if rand_mode == "first" else oracle.RAND_SEEDED,
                           error_feedback=ef)
-    _check_stats(ctx.stats(), ref)
+    st = ctx.stats()
+    _check_stats(st, ref)
     assert np.array_equal(_u32(idx), ref.sel.idx)
     assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32))
     if ef:
@@ -66,7 +67,11 @@ def _compress_case(tk, d, dist, k, N, *, ef=True, seed=0, step=0, rank=0, rand_m
     else:
         assert np.array_equal(_f32bits(gd), g.view(np.uint32))  # g never written
     ctx.close()
+    _PATHS.add(st.compacted)
     return ref
+
+
+_PATHS = set()  # which selection paths (compacted / whole-vector) the parity cases exercised
 
 
 EDGE_D = [1, 2, 3, 4, 5, 127, 128, 129, 511, 4095, 4096, 4097, 8191, 12289, (1 << 20) + 3]
@@ -92,6 +97,14 @@ def test_compress_levels_per_pass_invariance(tk, levels, N):
 @pytest.mark.parametrize("k", [1, 2, 999, 10000])
 def test_compress_k_extremes(tk, k):
     _compress_case(tk, 10000, "H", k, 10, seed=9)
+
+
+def test_both_selection_paths_exercised(tk):
+    # a typical case takes the compacted path; k = d / a low bracket forces the whole-vector path
+    _compress_case(tk, 100_000, "G", 100, 10)
+    _compress_case(tk, 100_000, "G", 60_000, 10)
+    _compress_case(tk, 100_000, "H", 100_000, 10)
+    assert _PATHS == {True, False}
 
 
 def test_compress_no_error_feedback_and_first_mode(tk):
