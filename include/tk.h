@@ -42,7 +42,8 @@ typedef enum tk_status {
   TK_ERR_INVALID_ARG = 1, /* NULL / misaligned pointer, d == 0 or d >= 2^32, rho not in (0,1],
                              N not in [1,52], rank >= P, aliasing buffers                    */
   TK_ERR_RANGE = 2,       /* explicit k not in [1, d] (segment length for HiTopKComm)          */
-  TK_ERR_CONFIG = 3,      /* P % n != 0, d % n != 0, NCCL unique id missing for P > 1          */
+  TK_ERR_CONFIG = 3,      /* P % n != 0, d % n != 0, (d/n) % 4 != 0 for n > 1 (segments must be
+                             16-byte aligned), NCCL unique id missing for P > 1               */
   TK_ERR_NONFINITE = 4,   /* NaN/Inf met in acc (precondition, Q24); sticky, reported by the
                              next tk_get_stats                                                 */
   TK_ERR_CUDA = 5,        /* CUDA runtime error; text in tk_last_error                        */
@@ -53,6 +54,11 @@ typedef enum tk_status {
 
 enum { TK_RAND_SEEDED = 0, TK_RAND_FIRST = 1 };   /* Alg. 1 l.27 window start (Q10)           */
 enum { TK_STEP4_DENSE = 0, TK_STEP4_SPARSE = 1 }; /* HiTopKComm step 4: Alg. 2 l.21-23 vs Eq.10*/
+enum { TK_RS_ORDERED = 0, TK_RS_NCCL = 1 };       /* HiTopKComm step 1 reduce-scatter (Q20):
+                                                     ORDERED = ascending-row-rank fp32 sum read over
+                                                     NVLink peer pointers inside the EF kernel
+                                                     (bit-exact; n in {2,4,8});
+                                                     NCCL = ncclReduceScatter (order unspecified) */
 
 typedef struct tk_config {
   uint64_t d;              /* gradient length (the paper's d)                           */
@@ -70,6 +76,7 @@ typedef struct tk_config {
   uint32_t levels_per_pass;/* bisection levels resolved per count pass over the data (1..4;
                               0 = default 3).  Result bits do not depend on it.               */
   int32_t device;          /* CUDA device ordinal to use (-1 = current)                        */
+  uint32_t rs_mode;        /* HiTopKComm step-1 mode (TK_RS_ORDERED or TK_RS_NCCL)             */
 } tk_config;
 
 /* Snapshot of the last compression's MSTopK control block (for parity checks). */
@@ -136,6 +143,11 @@ tk_status tk_step(tk_ctx* ctx, const float* g, float* r, float* out, uint32_t* g
  * and copies the P*2k gathered pairs (flat) back to gathered_host and, if out_host != NULL, the
  * dense aggregate back to out_host.  Synchronises the context stream. */
 tk_status tk_step_host(tk_ctx* ctx, const float* g_host, uint32_t* gathered_host, float* out_host);
+
+/* HiTopKComm with TK_RS_ORDERED: the context's peer-visible gradient buffer ([d] fp32, device).
+ * A caller that writes its gradient here and passes this pointer as g to tk_step avoids the
+ * copy-in (tk_step copies any other g into it first).  NULL for flat mode. */
+tk_status tk_input_buffer(tk_ctx* ctx, float** g);
 
 /* Copy the control block of the last compression to *st (synchronises the stream). */
 tk_status tk_get_stats(tk_ctx* ctx, tk_stats* st);

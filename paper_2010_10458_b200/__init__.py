@@ -38,7 +38,7 @@ class _Config(ctypes.Structure):
                 ("n_iters", ctypes.c_uint32), ("nranks", ctypes.c_uint32), ("rank", ctypes.c_uint32),
                 ("group_size", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("rand_mode", ctypes.c_uint32),
                 ("error_feedback", ctypes.c_uint32), ("step4", ctypes.c_uint32),
-                ("levels_per_pass", ctypes.c_uint32), ("device", ctypes.c_int32)]
+                ("levels_per_pass", ctypes.c_uint32), ("device", ctypes.c_int32), ("rs_mode", ctypes.c_uint32)]
 
 
 class _Stats(ctypes.Structure):
@@ -57,7 +57,7 @@ class _Stats(ctypes.Structure):
 EXPORTS = ["tk_k", "tk_get_unique_id", "tk_init", "tk_compress", "tk_sparse_allgather", "tk_decompress",
            "tk_step", "tk_step_host", "tk_get_stats", "tk_set_step", "tk_query", "tk_launch_count",
            "tk_destroy", "tk_status_string", "tk_last_error", "tk_profile_begin", "tk_profile_end",
-           "tk_stage_name"]
+           "tk_stage_name", "tk_input_buffer"]
 NSTAGES = 16
 
 
@@ -87,6 +87,7 @@ def _load():
         "tk_profile_begin": (I32, [P, U32]),
         "tk_profile_end": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(U32)]),
         "tk_stage_name": (ctypes.c_char_p, [U32]),
+        "tk_input_buffer": (I32, [P, ctypes.POINTER(P)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -169,6 +170,19 @@ class Stats:
     compacted: bool
 
 
+class _DeviceView:
+    """A float32 torch tensor aliasing libtk-owned device memory (via __cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int, device):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+        self.device = device
+
+    def tensor(self):
+        with torch.cuda.device(self.device):
+            return torch.as_tensor(self, device=self.device)
+
+
 class Context:
     """One rank's libtk context (tk_init).  ``d, rho, n_iters`` follow the paper's statement of
     the problem (x in R^d, k = rho*d, N samplings, P workers, m x n for HiTopKComm)."""
@@ -176,7 +190,7 @@ class Context:
     def __init__(self, d: int, rho: float = 0.001, n_iters: int = 10, *, k: int = 0, nranks: int = 1, rank: int = 0,
                  group_size: int = 1, seed: int = 0, rand_mode: str = "seeded", error_feedback: bool = True,
                  step4: str = "dense", levels_per_pass: int = 0, device: int | None = None, uid: bytes | None = None,
-                 stream: torch.cuda.Stream | None = None):
+                 stream: torch.cuda.Stream | None = None, rs_mode: str = "ordered"):
         if not torch.cuda.is_available():
             raise RuntimeError("libtk needs a CUDA device (B200, sm_100a); there is no CPU fallback")
         dev = torch.cuda.current_device() if device is None else int(device)
@@ -185,7 +199,8 @@ class Context:
         cfg = _Config(d=int(d), rho=float(rho), k=int(k), n_iters=int(n_iters), nranks=int(nranks), rank=int(rank),
                       group_size=int(group_size), seed=int(seed) & ((1 << 64) - 1),
                       rand_mode={"seeded": 0, "first": 1}[rand_mode], error_feedback=1 if error_feedback else 0,
-                      step4={"dense": 0, "sparse": 1}[step4], levels_per_pass=int(levels_per_pass), device=dev)
+                      step4={"dense": 0, "sparse": 1}[step4], levels_per_pass=int(levels_per_pass), device=dev,
+                      rs_mode={"ordered": 0, "nccl": 1}[rs_mode])
         self._ctx = ctypes.c_void_p()
         if nranks > 1 and uid is None:
             raise ValueError("nranks > 1 needs the NCCL unique id (broadcast_unique_id())")
@@ -265,6 +280,16 @@ class Context:
                      thres2=s.thres2, thres1_set=bool(s.thres1_set), thres2_set=bool(s.thres2_set), key1=s.key1,
                      key2=s.key2, len2=s.len2, rand=s.rand_start, step=s.step, nonfinite=bool(s.nonfinite),
                      compacted=bool(s.compacted))
+
+    def input_buffer(self):
+        """HiTopKComm ordered mode: a torch view of libtk's peer-visible gradient buffer (write the
+        gradient here and pass it as g to step() to skip the copy-in); None in flat mode."""
+        p = ctypes.c_void_p()
+        self._check(_lib.tk_input_buffer(self._ctx, ctypes.byref(p)))
+        if not p.value:
+            return None
+        # wrap the device pointer without copying (the buffer lives as long as the context)
+        return _DeviceView(p.value, self.d, self.device).tensor()
 
     def set_step(self, step: int):
         self._check(_lib.tk_set_step(self._ctx, int(step)))

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "tk.h"
 #include "tk_kernels.cuh"
@@ -52,6 +53,9 @@ struct tk_ctx {
   float* h_r = nullptr;
   float* h_out = nullptr;
   ncclComm_t world = nullptr, row = nullptr, col = nullptr;
+  float* sym_g = nullptr;             // HiTopKComm ordered RS: this GPU's peer-visible gradient [d]
+  float* peer_g[8] = {nullptr};       // row peers' sym_g (IPC-opened; [row_pos] = sym_g)
+  int32_t* sync_buf = nullptr;        // 4-byte buffer of the row barrier all-reduce
   uint64_t step = 0;
   uint64_t launches = 0;
   uint32_t nonfinite_sticky = 0;
@@ -133,16 +137,31 @@ tk_status launch_count(tk_ctx* c, const float* acc, const SearchParams& sp, int 
   return s;
 }
 
-// MSTopK on a vector of length L (= c->L) with error feedback: g (+ r) -> idx/val.
-tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, float* val) {
+template <bool EF, int NP>
+void launch_ef(tk_ctx* c, const float* g, const Peers& pr, float* r, const SearchParams& sp) {
+  k_ef_stats<EF, NP><<<c->grid_stats, THREADS, 0, c->stream>>>(g, pr, r, sp, c->units_per_warp, c->cta_sum,
+                                                               c->cta_max, c->ctrl, c->step, c->lev_sched[0]);
+}
+
+// MSTopK on a vector of length L (= c->L) with error feedback: g (+ r) -> idx/val.  With
+// peers != nullptr the gradient is the ordered sum of the np peer segments (HiTopKComm step 1).
+tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, float* val, const Peers* peers = nullptr,
+                        int np = 0) {
   const bool ef = c->cfg.error_feedback != 0;
   const SearchParams sp = search_params(c);
-  if (ef) {
-    k_ef_stats<true><<<c->grid_stats, THREADS, 0, c->stream>>>(g, r, sp, c->units_per_warp, c->cta_sum, c->cta_max,
-                                                               c->ctrl, c->step, c->lev_sched[0]);
-  } else {
-    k_ef_stats<false><<<c->grid_stats, THREADS, 0, c->stream>>>(g, nullptr, sp, c->units_per_warp, c->cta_sum,
-                                                                c->cta_max, c->ctrl, c->step, c->lev_sched[0]);
+  Peers pr;
+  memset(&pr, 0, sizeof(pr));
+  if (peers) pr = *peers;
+  switch ((ef ? 100 : 0) + np) {
+    case 100: launch_ef<true, 0>(c, g, pr, r, sp); break;
+    case 102: launch_ef<true, 2>(c, g, pr, r, sp); break;
+    case 104: launch_ef<true, 4>(c, g, pr, r, sp); break;
+    case 108: launch_ef<true, 8>(c, g, pr, r, sp); break;
+    case 0: launch_ef<false, 0>(c, g, pr, nullptr, sp); break;
+    case 2: launch_ef<false, 2>(c, g, pr, nullptr, sp); break;
+    case 4: launch_ef<false, 4>(c, g, pr, nullptr, sp); break;
+    case 8: launch_ef<false, 8>(c, g, pr, nullptr, sp); break;
+    default: return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
   }
   TK_TRY(check_launch(c, "k_ef_stats"));
   mark(c, TK_STAGE_EF_STATS);
@@ -196,7 +215,7 @@ tk_status plan_launches(tk_ctx* c) {
   TK_CUDA(c, cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, c->device));
   c->sms = (uint32_t)v;
   int o1 = 0, o2 = 0, o3 = 0, o4 = 0, o5 = 0, o6 = 0, o7 = 0;
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_ef_stats<true>, THREADS, 0));
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_ef_stats<true, 0>, THREADS, 0));
   TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_count<2, true>, THREADS, 0));
   TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_count<2, false>, THREADS, 0));
   TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_count<3, false>, THREADS, 0));
@@ -229,6 +248,40 @@ tk_status plan_launches(tk_ctx* c) {
   return TK_OK;
 }
 
+// HiTopKComm ordered reduce-scatter: every GPU exposes a gradient buffer to its row peers through
+// CUDA IPC; the 64-byte handles are exchanged with an all-gather on the row communicator.
+tk_status open_row_peers(tk_ctx* c) {
+  TK_TRY(dev_alloc(c, &c->sym_g, c->d));
+  TK_TRY(dev_alloc(c, &c->sync_buf, 1));
+  TK_CUDA(c, cudaMemset(c->sync_buf, 0, sizeof(int32_t)));
+  cudaIpcMemHandle_t mine;
+  TK_CUDA(c, cudaIpcGetMemHandle(&mine, c->sym_g));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  char* dev = nullptr;
+  TK_TRY(dev_alloc(c, &dev, 64 * (size_t)(c->n + 1)));
+  TK_CUDA(c, cudaMemcpy(dev, &mine, 64, cudaMemcpyHostToDevice));
+  ncclResult_t r = ncclAllGather(dev, dev + 64, 64, ncclChar, c->row, c->stream);
+  if (r != ncclSuccess) {
+    cudaFree(dev);
+    return fail(c, TK_ERR_NCCL, "handle all-gather: %s", ncclGetErrorString(r));
+  }
+  std::vector<cudaIpcMemHandle_t> all(c->n);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess) e = cudaMemcpy(all.data(), dev + 64, 64 * (size_t)c->n, cudaMemcpyDeviceToHost);
+  cudaFree(dev);
+  if (e != cudaSuccess) return fail(c, TK_ERR_CUDA, "handle exchange: %s", cudaGetErrorString(e));
+  for (uint32_t q = 0; q < c->n; ++q) {
+    if (q == c->row_pos) {
+      c->peer_g[q] = c->sym_g;
+      continue;
+    }
+    void* p = nullptr;
+    TK_CUDA(c, cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess));
+    c->peer_g[q] = static_cast<float*>(p);
+  }
+  return TK_OK;
+}
+
 void free_all(tk_ctx* c) {
   void* ptrs[] = {c->cp.idx, c->cp.bits, c->cp.cnt, c->cta_sum, c->cta_max, c->wcnt, c->pre1, c->pre2, c->ctrl, c->send, c->recv,
                   c->recv_row, c->seg, c->h_g, c->h_r, c->h_out};
@@ -239,6 +292,10 @@ void free_all(tk_ctx* c) {
     delete[] c->prof_ev;
     delete[] c->prof_kind;
   }
+  for (uint32_t q = 0; q < 8; ++q)
+    if (c->peer_g[q] && c->peer_g[q] != c->sym_g) cudaIpcCloseMemHandle(c->peer_g[q]);
+  if (c->sym_g) cudaFree(c->sym_g);
+  if (c->sync_buf) cudaFree(c->sync_buf);
   if (c->row) ncclCommDestroy(c->row);
   if (c->col) ncclCommDestroy(c->col);
   if (c->world) ncclCommDestroy(c->world);
@@ -272,11 +329,13 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if (k.k == 0 && (!(k.rho > 0.0) || k.rho > 1.0)) return TK_ERR_INVALID_ARG;
   if (k.n_iters < 1 || k.n_iters > (uint32_t)NMAX) return TK_ERR_INVALID_ARG;
   if (k.nranks < 1 || k.rank >= k.nranks) return TK_ERR_INVALID_ARG;
-  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 4) return TK_ERR_INVALID_ARG;
+  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 4 || k.rs_mode > 1) return TK_ERR_INVALID_ARG;
   const uint32_t n = k.group_size == 0 ? 1 : k.group_size;
   if (k.nranks % n != 0) return TK_ERR_CONFIG;
   if (k.d % n != 0) return TK_ERR_CONFIG;
+  if (n > 1 && (k.d / n) % 4 != 0) return TK_ERR_CONFIG;  // segments start 16-byte aligned (128-bit access)
   if (k.nranks > 1 && !uid) return TK_ERR_CONFIG;
+  if (n > 1 && k.rs_mode == TK_RS_ORDERED && n != 2 && n != 4 && n != 8) return TK_ERR_CONFIG;
   const uint64_t L = k.d / n;
   uint64_t kk = k.k;
   if (kk == 0) kk = tk_k(L, k.rho);
@@ -330,7 +389,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   const uint32_t chunks_recv = (n == 1) ? c->P : c->m;
   if ((s = dev_alloc(c, &c->recv, (size_t)chunks_recv * 2 * kk)) != TK_OK) return bail(s);
   if (n > 1) {
-    if ((s = dev_alloc(c, &c->seg, L)) != TK_OK) return bail(s);
+    if (k.rs_mode == TK_RS_NCCL && (s = dev_alloc(c, &c->seg, L)) != TK_OK) return bail(s);
     if (k.step4 == TK_STEP4_SPARSE)
       if ((s = dev_alloc(c, &c->recv_row, (size_t)n * c->m * 2 * kk)) != TK_OK) return bail(s);
   }
@@ -345,6 +404,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
       if (c->m > 1 &&
           ncclCommSplit(c->world, (int)(c->rank % n), (int)c->rank, &c->col, nullptr) != ncclSuccess)
         return bail(TK_ERR_NCCL);
+      if (k.rs_mode == TK_RS_ORDERED && (s = open_row_peers(c)) != TK_OK) return bail(s);
     }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(TK_ERR_CUDA);
@@ -415,11 +475,28 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
     mark(c, TK_STAGE_ALLGATHER);
     TK_TRY(decompress_impl(c, gat, c->P, c->k, c->d, out));
   } else {
-    // HiTopKComm (Alg. 2).  Step 1: intra-node reduce-scatter of g (Eq. 4).
-    TK_NCCL(c, ncclReduceScatter(g, c->seg, c->L, ncclFloat32, ncclSum, c->row, c->stream));
-    mark(c, TK_STAGE_REDUCE_SCATTER);
-    // Step 2: MSTopK on the segment with k~ (Eq. 5), error feedback on the segment residual.
-    TK_TRY(compress_impl(c, c->seg, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k)));
+    // HiTopKComm (Alg. 2).  Step 1: intra-node reduce-scatter of g (Eq. 4) ...
+    if (c->cfg.rs_mode == TK_RS_ORDERED) {
+      // ... ordered, read by this GPU's EF kernel straight from the row peers' buffers: make g
+      // peer-visible, then a row barrier (stream-ordered all-reduce of 4 bytes) so every peer's
+      // copy is complete before anyone reads it.  The previous step's row all-gather (step 4)
+      // already ordered every peer's last read of these buffers before this copy.
+      if (g != c->sym_g)
+        TK_CUDA(c, cudaMemcpyAsync(c->sym_g, g, sizeof(float) * c->d, cudaMemcpyDeviceToDevice, c->stream));
+      TK_NCCL(c, ncclAllReduce(c->sync_buf, c->sync_buf, 1, ncclInt32, ncclSum, c->row, c->stream));
+      mark(c, TK_STAGE_REDUCE_SCATTER);
+      Peers pr;
+      memset(&pr, 0, sizeof(pr));
+      for (uint32_t q = 0; q < c->n; ++q) pr.p[q] = c->peer_g[q] + (size_t)c->row_pos * c->L;
+      // Step 2 (fused with step 1): MSTopK on the segment with k~ (Eq. 5), EF on the segment residual.
+      TK_TRY(compress_impl(c, nullptr, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k), &pr,
+                           (int)c->n));
+    } else {
+      TK_NCCL(c, ncclReduceScatter(g, c->seg, c->L, ncclFloat32, ncclSum, c->row, c->stream));
+      mark(c, TK_STAGE_REDUCE_SCATTER);
+      // Step 2: MSTopK on the segment with k~ (Eq. 5), error feedback on the segment residual.
+      TK_TRY(compress_impl(c, c->seg, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k)));
+    }
     // Step 3: inter-node all-gather among the m GPUs at the same position j (Eq. 6) ...
     uint32_t* gat = gathered ? gathered : c->recv;
     if (c->m > 1) {
@@ -468,6 +545,12 @@ tk_status tk_step_host(tk_ctx* c, const float* g_host, uint32_t* gathered_host, 
   if (out_host)
     TK_CUDA(c, cudaMemcpyAsync(out_host, c->h_out, sizeof(float) * c->d, cudaMemcpyDeviceToHost, c->stream));
   TK_CUDA(c, cudaStreamSynchronize(c->stream));
+  return TK_OK;
+}
+
+tk_status tk_input_buffer(tk_ctx* c, float** g) {
+  if (!c || !g) return TK_ERR_INVALID_ARG;
+  *g = c->sym_g;
   return TK_OK;
 }
 

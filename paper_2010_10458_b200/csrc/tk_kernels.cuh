@@ -265,18 +265,58 @@ __device__ void stats_finalize(Ctrl* c, const SearchParams& sp, double S, uint32
   c->cmp_ratio = c->cand_ratio[ms];
 }
 
-template <bool EF>
-__device__ __forceinline__ void ef_load(const float* g, const float* r, uint64_t base, float4* gv, float4* rv) {
+// HiTopKComm step 1 fused into K1 (Eq. 4; reading Q20): with NP > 0 the gradient of
+// this GPU's segment is the ordered reduce-scatter sum_{q=0..NP-1} g_q[segment], read directly
+// from the row peers' memory (CUDA IPC peer pointers over NVLink) and added in ascending row rank,
+// left to right, in fp32 round-to-nearest - bit-exact, unlike a reduce-scatter whose order the
+// library chooses.
+struct Peers {
+  const float* p[8];  // row peers' gradient + segment offset, in row-rank order
+};
+
+template <int NP>
+__device__ __forceinline__ void load_g(const float* g, const Peers& pr, uint64_t base, float4* gv) {
+  if (NP == 0) {
 #pragma unroll
-  for (int ch = 0; ch < 4; ++ch) gv[ch] = __ldcs(reinterpret_cast<const float4*>(g + base + ch * 128));
+    for (int ch = 0; ch < 4; ++ch) gv[ch] = __ldcs(reinterpret_cast<const float4*>(g + base + ch * 128));
+  } else {
+    float4 pv[NP > 0 ? NP : 1][4];
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) pv[q][ch] = __ldcs(reinterpret_cast<const float4*>(pr.p[q] + base + ch * 128));
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      float4 a = pv[0][ch];
+#pragma unroll
+      for (int q = 1; q < NP; ++q)
+        a = make_float4(__fadd_rn(a.x, pv[q][ch].x), __fadd_rn(a.y, pv[q][ch].y), __fadd_rn(a.z, pv[q][ch].z),
+                        __fadd_rn(a.w, pv[q][ch].w));
+      gv[ch] = a;
+    }
+  }
+}
+template <int NP>
+__device__ __forceinline__ float load_g1(const float* g, const Peers& pr, uint64_t i) {
+  if (NP == 0) return g[i];
+  float a = pr.p[0][i];
+#pragma unroll
+  for (int q = 1; q < NP; ++q) a = __fadd_rn(a, pr.p[q][i]);
+  return a;
+}
+
+template <bool EF, int NP>
+__device__ __forceinline__ void ef_load(const float* g, const Peers& pr, const float* r, uint64_t base, float4* gv,
+                                        float4* rv) {
+  load_g<NP>(g, pr, base, gv);
   if (EF) {
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) rv[ch] = __ldcs(reinterpret_cast<const float4*>(r + base + ch * 128));
   }
 }
 
-template <bool EF>
-__global__ void __launch_bounds__(THREADS, 4) k_ef_stats(const float* __restrict__ g, float* __restrict__ r,
+template <bool EF, int NP>
+__global__ void __launch_bounds__(THREADS, 4) k_ef_stats(const float* __restrict__ g, Peers pr, float* __restrict__ r,
                                                          SearchParams sp, uint32_t units_per_warp,
                                                          double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max,
                                                          Ctrl* __restrict__ c, uint64_t step, int first_levels) {
@@ -293,7 +333,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_ef_stats(const float* __restrict
     float4 acc[4];
     if ((u + 1) * ROUND <= n) {
       float4 rv[4];
-      ef_load<EF>(g, r, base, acc, rv);
+      ef_load<EF, NP>(g, pr, r, base, acc, rv);
       if (EF) {
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
@@ -311,7 +351,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_ef_stats(const float* __restrict
           const uint64_t idx = base + ch * 128 + e;
           float x = 0.0f;  // zero leaves beyond n (padding of the canonical tree)
           if (idx < n) {
-            x = g[idx];
+            x = load_g1<NP>(g, pr, idx);
             if (EF) {
               x = __fadd_rn(x, r[idx]);
               r[idx] = x;
