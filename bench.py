@@ -201,7 +201,7 @@ def cpu_baseline(a, P, budget_s=15.0):
                       f"EF; {total:.1f} s of CPU work; host has {host_cores()} cores"}
 
 
-def run_reference(a, ws, rank):
+def run_reference(a, ws, rank, emit):
     if rank != 0:
         return
     P = ws
@@ -221,7 +221,7 @@ def run_reference(a, ws, rank):
                              "sample": f"each step: the whole {P}-rank step simulated in one process on d={d_s} per rank "
                                        f"(bounded sample of d={a.d}); numpy, 1 thread; host has {host_cores()} cores"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------------------------------ libtk arm
@@ -240,11 +240,23 @@ def stage_bytes(name, L, d, k, P, ef, chunks):
     return None
 
 
+def log(*x):
+    print(f"[bench {time.strftime('%H:%M:%S')}]", *x, file=sys.stderr, flush=True)
+
+
 def main():
+    # C-level stdout (e.g. NCCL's version banner) goes to stderr: stdout carries exactly one JSON line
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+
+    def emit(obj):
+        os.write(json_fd, (json.dumps(obj) + "\n").encode())
+
     a = parse()
     ws, rank, local = dist_setup(a)
+    log("rank", rank, "of", ws, "up")
     if a.impl == "reference":
-        run_reference(a, ws, rank)
+        run_reference(a, ws, rank, emit)
         if ws > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
@@ -259,6 +271,7 @@ def main():
     ctx = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, nranks=P, rank=rank, group_size=n, seed=2010_10458,
                      step4=a.step4, levels_per_pass=a.levels, uid=uid, stream=stream, device=local)
     L, k = ctx.seg_len, ctx.k
+    log("ctx up")
     # inputs: a fresh seeded N(0,1) gradient for every warm-up / timed / profiled step, generated on
     # the device before any timing (pool capped at ~16 GB per rank; reused cyclically beyond that)
     need = a.warmup + 2 * a.steps
@@ -275,6 +288,7 @@ def main():
         out = torch.empty(a.d, dtype=torch.float32, device="cuda")
     stream.synchronize()
     cursor = [0]
+    log("inputs generated")
 
     def run(steps, rr=None):
         rr = r if rr is None else rr
@@ -285,13 +299,19 @@ def main():
     sampler = None if a.ncu else ClockSampler(local)
     if not a.ncu:
         # keep the GPU under this load ~1 s (on a scratch residual) so the clock samples describe
-        # the timed region's regime
-        t_end = time.time() + 1.0
+        # the timed region's regime; every rank runs the same number of steps (collectives match)
+        torch.cuda.synchronize()
+        t0 = time.time()
         with torch.cuda.stream(stream):
-            while time.time() < t_end:
-                run(20, r_soak)
+            run(50, r_soak)
+        stream.synchronize()
+        per = max_over_ranks((time.time() - t0) / 50, ws)
+        n_soak = int(min(20000, max(10, 1.0 / max(per, 1e-6))))
+        with torch.cuda.stream(stream):
+            for i in range(0, n_soak, 50):
+                run(min(50, n_soak - i), r_soak)
                 stream.synchronize()
-    # the measured error-feedback run starts from r = 0 at step 0 with fresh gradients
+    log("soak done")
     cursor[0] = 0
     ctx.set_step(0)
     with torch.cuda.stream(stream):
@@ -310,6 +330,7 @@ def main():
     torch.cuda.synchronize()
     barrier(ws)
     clocks = sampler.stop() if sampler else None
+    log("timed region done")
     launches = ctx.launches - l0
     t_step = max_over_ranks(e0.elapsed_time(e1) / a.steps, ws)  # ms, max over ranks
     gpu_launches = int(sum_over_ranks(launches, ws))
@@ -320,6 +341,7 @@ def main():
     with torch.cuda.stream(stream):
         run(a.steps)
     prof = ctx.profile_end()
+    log("profile done")
     chunks = P if n == 1 else P // n
     stages = {}
     for name, (ms, cnt) in prof.items():
@@ -361,6 +383,7 @@ def main():
         for i in range(ks):
             ctx_h.step_host(hg[i % 2], gat_h)
         t_e2e = max_over_ranks((time.perf_counter() - t0) / ks, ws)
+        log("e2e done")
         e2e = {"value": P * a.d / t_e2e, "unit": UNIT, "ms_per_step": t_e2e * 1e3,
                "h2d_bytes_per_step": 4 * a.d, "d2h_bytes_per_step": 4 * chunks * 2 * k,
                "api": "tk_step_host (pinned host gradient in, gathered (index, value) pairs out; residual device-resident)"}
@@ -382,7 +405,7 @@ def main():
                                  f"{12 * a.d / 1e6:.0f} MB per rank per step vs 126 MB L2; no explicit flush"},
                 "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "stages": stages}
-        print(json.dumps(line), flush=True)
+        emit(line)
     ctx.close()
     if ws > 1:
         import torch.distributed as dist
