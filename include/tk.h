@@ -73,8 +73,10 @@ typedef struct tk_config {
   uint32_t error_feedback; /* 1: acc = g + r, r' = acc with sent entries := +0.0 (Q14);
                               0: MSTopK runs on g itself and r is ignored (may be NULL)         */
   uint32_t step4;          /* HiTopKComm step 4 mode (TK_STEP4_DENSE or TK_STEP4_SPARSE)       */
-  uint32_t levels_per_pass;/* bisection levels resolved per count pass over the data (1..4;
-                              0 = default 3).  Result bits do not depend on it.               */
+  uint32_t levels_per_pass;/* bisection levels resolved per count pass (1..8; 0 = default 8): the
+                              first pass over the whole vector resolves min(2, this); later passes
+                              on the compacted entries resolve up to this many at once, passes
+                              over the whole vector up to 2.  Result bits do not depend on it.  */
   int32_t device;          /* CUDA device ordinal to use (-1 = current)                        */
   uint32_t rs_mode;        /* HiTopKComm step-1 mode (TK_RS_ORDERED or TK_RS_NCCL)             */
 } tk_config;
@@ -98,6 +100,10 @@ typedef struct tk_stats {
   uint32_t nonfinite;      /* 1 if a NaN/Inf was seen (sticky)                                 */
   uint32_t compacted;      /* 1 if passes 2.. and the selection ran on the entries compacted by
                               the first count pass (an exact shortcut)          */
+  uint32_t n_phases;       /* phase boundaries recorded in phase_ns                             */
+  uint64_t phase_ns[8];    /* device %globaltimer (ns) at k_compress's phase boundaries (CTA 0,
+                              after each grid barrier): start, stats, each count pass, prefix,
+                              end of selection                                                 */
 } tk_stats;
 
 /* k = max(1, floor(rho * d)) in fp64 (Q13).  Host-only, pure.  0 on invalid input. */
@@ -165,12 +171,12 @@ uint64_t tk_launch_count(const tk_ctx* ctx);
 /* Stage profiling with CUDA events on the context stream.  Between tk_profile_begin and
  * tk_profile_end every tk_step records an event at each stage boundary (capacity max_steps
  * steps).  tk_profile_end synchronises and returns, per stage, the summed device time in ms and
- * the number of launches (ms / launches = mean duration of one launch of that stage). */
+ * the number of launches (ms / launches = mean duration of one launch of that stage).  Stages:
+ * k_compress (A1-A8 in one cooperative kernel), allgather (NCCL or the P = 1 copy),
+ * k_decompress, reduce_scatter (HiTopKComm step-1 barrier or NCCL RS), step4_allgather. */
 enum {
-  TK_STAGE_NONE = 0, TK_STAGE_EF_STATS = 1, TK_STAGE_FINALIZE = 2, TK_STAGE_COUNT1 = 3, TK_STAGE_COUNT3 = 4,
-  TK_STAGE_COUNT7 = 5, TK_STAGE_COUNT15 = 6, TK_STAGE_SCAN = 7, TK_STAGE_SELECT = 8, TK_STAGE_ALLGATHER = 9,
-  TK_STAGE_TILE_RANGES = 10, TK_STAGE_DECOMPRESS = 11, TK_STAGE_REDUCE_SCATTER = 12,
-  TK_STAGE_STEP4_ALLGATHER = 13, TK_NSTAGES = 16
+  TK_STAGE_NONE = 0, TK_STAGE_COMPRESS = 1, TK_STAGE_ALLGATHER = 9, TK_STAGE_DECOMPRESS = 11,
+  TK_STAGE_REDUCE_SCATTER = 12, TK_STAGE_STEP4_ALLGATHER = 13, TK_NSTAGES = 16
 };
 tk_status tk_profile_begin(tk_ctx* ctx, uint32_t max_steps);
 tk_status tk_profile_end(tk_ctx* ctx, double ms[TK_NSTAGES], uint32_t launches[TK_NSTAGES]);

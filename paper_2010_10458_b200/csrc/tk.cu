@@ -30,19 +30,20 @@ struct tk_ctx {
   uint32_t row_pos = 0, col_pos = 0;  // j = rank % n (position in the node), i = rank / n (node)
   uint64_t d = 0, L = 0, k = 0;       // L = d / n (segment length); k = k (flat) or k~ (HiTopK)
   uint32_t sms = 148;
-  uint32_t grid_stats = 0;            // K1 CTAs
-  uint32_t grid_slab = 0;             // K2/K4 CTAs (their warps partition [0, L) into slabs)
+  uint32_t grid = 0;                  // CTAs of the cooperative compression kernel
   uint32_t W = 0;                     // warp slabs
   uint64_t S = 0;                     // slab length
   uint32_t occ_dec = 1;               // resident decompression CTAs per SM
   uint32_t levels = 4, npass = 0;
   int lev_sched[NMAX];
-  uint32_t units_per_warp = 1;        // K1: aligned power-of-two run of 512-element units per warp
+  uint32_t units_per_warp = 1;        // ef phase: aligned power-of-two run of 512-element units per warp
+  uint32_t* cta_cls = nullptr;        // [2][grid] per-CTA class counts
+  uint32_t* totals = nullptr;         // [npass][16] trial totals
+  uint32_t* bar = nullptr;            // grid barrier words [2] + flags [2]
+  uint32_t* flags = nullptr;
   double* cta_sum = nullptr;          // K1 per-CTA partial sums / maxima
   uint32_t* cta_max = nullptr;
   uint32_t* wcnt = nullptr;           // per-warp-slab counts [npass*TMAX][W]
-  uint32_t* pre1 = nullptr;           // per-slab exclusive prefix of class-1 / class-2 counts
-  uint32_t* pre2 = nullptr;
   Compact cp;                         // compacted entries of the first count pass
   Ctrl* ctrl = nullptr;
   uint32_t* send = nullptr;      // [2k]
@@ -128,62 +129,58 @@ SearchParams search_params(const tk_ctx* c) {
   return sp;
 }
 
-template <int LEV, bool FIRST>
-tk_status launch_count(tk_ctx* c, const float* acc, const SearchParams& sp, int pass, int next_lev) {
-  k_count<LEV, FIRST><<<c->grid_slab, THREADS, 0, c->stream>>>(acc, c->ctrl, sp, c->wcnt, c->pre1, c->pre2, c->cp,
-                                                                pass, next_lev);
-  tk_status s = check_launch(c, "k_count");
-  mark(c, LEV == 1 ? TK_STAGE_COUNT1 : LEV == 2 ? TK_STAGE_COUNT3 : LEV == 3 ? TK_STAGE_COUNT7 : TK_STAGE_COUNT15);
-  return s;
+const void* compress_kernel(bool ef, int np) {
+  switch ((ef ? 100 : 0) + np) {
+    case 100: return reinterpret_cast<const void*>(&k_compress<true, 0>);
+    case 102: return reinterpret_cast<const void*>(&k_compress<true, 2>);
+    case 104: return reinterpret_cast<const void*>(&k_compress<true, 4>);
+    case 108: return reinterpret_cast<const void*>(&k_compress<true, 8>);
+    case 0: return reinterpret_cast<const void*>(&k_compress<false, 0>);
+    case 2: return reinterpret_cast<const void*>(&k_compress<false, 2>);
+    case 4: return reinterpret_cast<const void*>(&k_compress<false, 4>);
+    case 8: return reinterpret_cast<const void*>(&k_compress<false, 8>);
+  }
+  return nullptr;
 }
 
-template <bool EF, int NP>
-void launch_ef(tk_ctx* c, const float* g, const Peers& pr, float* r, const SearchParams& sp) {
-  k_ef_stats<EF, NP><<<c->grid_stats, THREADS, 0, c->stream>>>(g, pr, r, sp, c->units_per_warp, c->cta_sum,
-                                                               c->cta_max, c->ctrl, c->step, c->lev_sched[0]);
-}
+int peer_sources(const tk_ctx* c) { return (c->n > 1 && c->cfg.rs_mode == TK_RS_ORDERED) ? (int)c->n : 0; }
 
-// MSTopK on a vector of length L (= c->L) with error feedback: g (+ r) -> idx/val.  With
-// peers != nullptr the gradient is the ordered sum of the np peer segments (HiTopKComm step 1).
+// MSTopK on a vector of length L (= c->L) with error feedback: g (+ r) -> idx/val, as ONE
+// cooperative launch of k_compress.  With peers != nullptr the gradient is the ordered sum of the
+// np peer segments (HiTopKComm step 1).
 tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, float* val, const Peers* peers = nullptr,
                         int np = 0) {
   const bool ef = c->cfg.error_feedback != 0;
-  const SearchParams sp = search_params(c);
-  Peers pr;
-  memset(&pr, 0, sizeof(pr));
-  if (peers) pr = *peers;
-  switch ((ef ? 100 : 0) + np) {
-    case 100: launch_ef<true, 0>(c, g, pr, r, sp); break;
-    case 102: launch_ef<true, 2>(c, g, pr, r, sp); break;
-    case 104: launch_ef<true, 4>(c, g, pr, r, sp); break;
-    case 108: launch_ef<true, 8>(c, g, pr, r, sp); break;
-    case 0: launch_ef<false, 0>(c, g, pr, nullptr, sp); break;
-    case 2: launch_ef<false, 2>(c, g, pr, nullptr, sp); break;
-    case 4: launch_ef<false, 4>(c, g, pr, nullptr, sp); break;
-    case 8: launch_ef<false, 8>(c, g, pr, nullptr, sp); break;
-    default: return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
-  }
-  TK_TRY(check_launch(c, "k_ef_stats"));
-  mark(c, TK_STAGE_EF_STATS);
-  const float* acc = ef ? r : g;
-  for (uint32_t p = 0; p < c->npass; ++p) {
-    const int next = (p + 1 < c->npass) ? c->lev_sched[p + 1] : 0;
-    if (p == 0) {
-      if (c->lev_sched[0] == 1) TK_TRY((launch_count<1, true>(c, acc, sp, 0, next)));
-      else TK_TRY((launch_count<2, true>(c, acc, sp, 0, next)));
-      continue;
-    }
-    switch (c->lev_sched[p]) {
-      case 1: TK_TRY((launch_count<1, false>(c, acc, sp, (int)p, next))); break;
-      case 2: TK_TRY((launch_count<2, false>(c, acc, sp, (int)p, next))); break;
-      case 3: TK_TRY((launch_count<3, false>(c, acc, sp, (int)p, next))); break;
-      default: TK_TRY((launch_count<4, false>(c, acc, sp, (int)p, next))); break;
-    }
-  }
-  k_select<<<c->grid_slab, THREADS, 0, c->stream>>>(acc, c->ctrl, sp, c->wcnt, c->pre1, c->pre2, idx, val,
-                                                    ef ? r : nullptr, c->cp);
-  TK_TRY(check_launch(c, "k_select"));
-  mark(c, TK_STAGE_SELECT);
+  Fused f;
+  memset(&f, 0, sizeof(f));
+  f.sp = search_params(c);
+  f.g = g;
+  if (peers) f.pr = *peers;
+  f.r = ef ? r : nullptr;
+  f.acc = ef ? r : g;
+  f.units_per_warp = c->units_per_warp;
+  f.cta_sum = c->cta_sum;
+  f.cta_max = c->cta_max;
+  f.wcnt = c->wcnt;
+  f.totals = c->totals;
+  f.cta_cls = c->cta_cls;
+  f.bar = c->bar;
+  f.flags = c->flags;
+  f.cp = c->cp;
+  f.idx_out = idx;
+  f.val_out = val;
+  f.c = c->ctrl;
+  f.step = c->step;
+  f.n_iters = c->cfg.n_iters;
+  f.lev0 = c->lev_sched[0];
+  f.cap_levels = (int)c->levels;
+  f.max_pass = (int)c->npass;
+  const void* kern = compress_kernel(ef, np);
+  if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
+  void* args[] = {&f};
+  TK_CUDA(c, cudaLaunchCooperativeKernel(kern, dim3(c->grid), dim3(THREADS), args, 0, c->stream));
+  TK_TRY(check_launch(c, "k_compress"));
+  mark(c, TK_STAGE_COMPRESS);
   return TK_OK;
 }
 
@@ -208,39 +205,36 @@ tk_status dev_alloc(tk_ctx* c, T** p, size_t count) {
   return TK_OK;
 }
 
-// Grid sizes (persistent: #SMs x resident CTAs), the warp-slab partition shared by the count
-// and selection kernels, and the hierarchical pairwise-sum partial arrays.
+// Grid of the cooperative compression kernel (#SMs x resident CTAs), the warp-slab partition of
+// the count and selection phases, the ef phase's units per warp, and the scratch they use.
 tk_status plan_launches(tk_ctx* c) {
   int v = 0;
   TK_CUDA(c, cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, c->device));
   c->sms = (uint32_t)v;
-  int o1 = 0, o2 = 0, o3 = 0, o4 = 0, o5 = 0, o6 = 0, o7 = 0;
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_ef_stats<true, 0>, THREADS, 0));
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_count<2, true>, THREADS, 0));
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_count<2, false>, THREADS, 0));
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, k_count<3, false>, THREADS, 0));
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o5, k_count<4, false>, THREADS, 0));
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o6, k_select, THREADS, 0));
+  int occ = 0, o7 = 0;
+  const void* kern = compress_kernel(c->cfg.error_feedback != 0, peer_sources(c));
+  if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count");
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0));
   TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o7, k_decompress, THREADS, 64 * sizeof(uint32_t)));
-  const uint32_t occ_slab = (uint32_t)std::max(1, std::min({o2, o3, o4, o5, o6}));
+  if (occ < 1) return fail(c, TK_ERR_CUDA, "k_compress cannot be resident");
   c->occ_dec = (uint32_t)std::max(1, o7);
   const uint64_t L = c->L;
-  // K1: each warp an aligned power-of-two run of 512-element units, grid <= resident CTAs
-  const uint64_t units = (L + ROUND - 1) / ROUND;
-  const uint64_t cap1 = (uint64_t)c->sms * std::max(1, o1);
-  uint64_t upw = 1;
-  while ((units + WARPS * upw - 1) / (WARPS * upw) > cap1) upw <<= 1;
-  c->units_per_warp = (uint32_t)upw;
-  c->grid_stats = (uint32_t)((units + WARPS * upw - 1) / (WARPS * upw));
-  // count / select: W warp slabs of S elements, S a multiple of ROUND
-  const uint64_t chunks = (L + ROUND - 1) / ROUND;
-  c->grid_slab = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sms * occ_slab,
-                                                                     (chunks + WARPS - 1) / WARPS));
-  c->W = c->grid_slab * WARPS;
+  const uint64_t rounds = (L + ROUND - 1) / ROUND;
+  // persistent cooperative grid: every CTA resident; no more CTAs than warp rounds of work
+  c->grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sms * occ, (rounds + WARPS - 1) / WARPS));
+  c->W = c->grid * WARPS;
   c->S = ((L + c->W - 1) / c->W + ROUND - 1) / ROUND * ROUND;  // whole rounds: no ragged slab ends
-  TK_TRY(dev_alloc(c, &c->cta_sum, c->grid_stats));
-  TK_TRY(dev_alloc(c, &c->cta_max, c->grid_stats));
-  // compacted entries: capacity S/4 per warp slab (the fallback path covers an overflow)
+  uint64_t upw = 1;  // ef phase: aligned power-of-two run of units per warp covering the vector
+  while ((uint64_t)c->W * upw < rounds) upw <<= 1;
+  c->units_per_warp = (uint32_t)upw;
+  TK_TRY(dev_alloc(c, &c->cta_sum, c->grid));
+  TK_TRY(dev_alloc(c, &c->cta_max, c->grid));
+  TK_TRY(dev_alloc(c, &c->cta_cls, 2 * (size_t)c->grid));
+  TK_TRY(dev_alloc(c, &c->totals, (size_t)HIST_BINS * c->npass));
+  TK_TRY(dev_alloc(c, &c->bar, 4));
+  TK_CUDA(c, cudaMemset(c->bar, 0, 4 * sizeof(uint32_t)));
+  c->flags = c->bar + 2;
+  // compacted entries: capacity S/4 per warp slab (the whole-vector path covers an overflow)
   c->cp.C = (uint32_t)std::max<uint64_t>(4, (c->S / 4 + 3) / 4 * 4);
   TK_TRY(dev_alloc(c, &c->cp.idx, (size_t)c->W * c->cp.C));
   TK_TRY(dev_alloc(c, &c->cp.bits, (size_t)c->W * c->cp.C));
@@ -283,7 +277,8 @@ tk_status open_row_peers(tk_ctx* c) {
 }
 
 void free_all(tk_ctx* c) {
-  void* ptrs[] = {c->cp.idx, c->cp.bits, c->cp.cnt, c->cta_sum, c->cta_max, c->wcnt, c->pre1, c->pre2, c->ctrl, c->send, c->recv,
+  void* ptrs[] = {c->cp.idx, c->cp.bits, c->cp.cnt, c->cta_sum, c->cta_max, c->cta_cls, c->totals, c->bar, c->wcnt,
+                  c->ctrl, c->send, c->recv,
                   c->recv_row, c->seg, c->h_g, c->h_r, c->h_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -329,7 +324,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if (k.k == 0 && (!(k.rho > 0.0) || k.rho > 1.0)) return TK_ERR_INVALID_ARG;
   if (k.n_iters < 1 || k.n_iters > (uint32_t)NMAX) return TK_ERR_INVALID_ARG;
   if (k.nranks < 1 || k.rank >= k.nranks) return TK_ERR_INVALID_ARG;
-  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 4 || k.rs_mode > 1) return TK_ERR_INVALID_ARG;
+  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 8 || k.rs_mode > 1) return TK_ERR_INVALID_ARG;
   const uint32_t n = k.group_size == 0 ? 1 : k.group_size;
   if (k.nranks % n != 0) return TK_ERR_CONFIG;
   if (k.d % n != 0) return TK_ERR_CONFIG;
@@ -355,19 +350,15 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   c->L = L;
   c->k = kk;
   c->stream = reinterpret_cast<cudaStream_t>(stream);
-  c->levels = k.levels_per_pass == 0 ? 4 : k.levels_per_pass;
-  // pass schedule: the first pass resolves min(2, levels) levels (its candidates spread over the
-  // whole [a-bar, u] range, where the full bucket search runs on every element); the remaining
-  // levels go in balanced passes of <= levels (their candidates bracket a narrow band, so most
-  // elements skip the search).  The result bits do not depend on the schedule.
+  c->levels = k.levels_per_pass == 0 ? 8 : k.levels_per_pass;
+  // pass schedule (decided on the device): the first pass resolves min(2, levels) levels on the
+  // whole vector; later passes take up to `levels` levels on the compacted entries, or up to 2 on
+  // the whole vector.  Scratch is sized for the worst case (all passes on the whole vector).
   {
     const uint32_t first = std::min<uint32_t>(std::min<uint32_t>(2u, c->levels), k.n_iters);
-    c->lev_sched[c->npass++] = (int)first;
-    const uint32_t rest = k.n_iters - first;
-    if (rest > 0) {
-      const uint32_t np = (rest + c->levels - 1) / c->levels;
-      for (uint32_t p = 0; p < np; ++p) c->lev_sched[c->npass++] = (int)(rest / np + (p < rest % np ? 1 : 0));
-    }
+    c->lev_sched[0] = (int)first;
+    const uint32_t per = std::min<uint32_t>(2u, c->levels);
+    c->npass = 1 + (k.n_iters - first + per - 1) / per;
   }
   auto bail = [&](tk_status s) {
     free_all(c);
@@ -382,8 +373,6 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   tk_status s;
   if ((s = plan_launches(c)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->wcnt, (size_t)c->npass * TMAX * c->W)) != TK_OK) return bail(s);
-  if ((s = dev_alloc(c, &c->pre1, c->W)) != TK_OK) return bail(s);
-  if ((s = dev_alloc(c, &c->pre2, c->W)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->ctrl, 1)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->send, 2 * kk)) != TK_OK) return bail(s);
   const uint32_t chunks_recv = (n == 1) ? c->P : c->m;
@@ -584,6 +573,8 @@ tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
   c->nonfinite_sticky |= h.nonfinite;
   st->nonfinite = c->nonfinite_sticky;
   st->compacted = h.cap_ok;
+  st->n_phases = std::min<uint32_t>(8, h.n_phase);
+  for (int i = 0; i < 8; ++i) st->phase_ns[i] = h.phase_ns[i];
   if (c->nonfinite_sticky) return fail(c, TK_ERR_NONFINITE, "non-finite value in acc (precondition, Q24)");
   return TK_OK;
 }
@@ -645,10 +636,10 @@ tk_status tk_profile_end(tk_ctx* c, double ms[TK_NSTAGES], uint32_t launches[TK_
 }
 
 const char* tk_stage_name(uint32_t stage) {
-  static const char* names[TK_NSTAGES] = {"none", "k_ef_stats", "k_finalize", "k_count<1>", "k_count<3>",
-                                          "k_count<7>", "k_count<15>", "k_scan", "k_select", "allgather",
-                                          "k_tile_ranges", "k_decompress", "reduce_scatter", "step4_allgather",
-                                          "reserved14", "reserved15"};
+  static const char* names[TK_NSTAGES] = {"none",      "k_compress", "reserved2",       "reserved3",
+                                          "reserved4", "reserved5",  "reserved6",       "reserved7",
+                                          "reserved8", "allgather",  "reserved10",      "k_decompress",
+                                          "reduce_scatter", "step4_allgather", "reserved14", "reserved15"};
   return stage < TK_NSTAGES ? names[stage] : "invalid";
 }
 

@@ -36,10 +36,9 @@ struct Ctrl {
   int32_t prov1, prov2;  // slot (pass*TMAX + candidate) whose per-warp counts are key1's / key2's; -1 unset
   uint32_t it;           // trials done
   uint32_t ncand;        // candidates of the pass about to run
-  uint32_t cand_key[16];
-  uint32_t totals[16];
-  double cand_ratio[16];
-  double cand_t[16];
+  uint32_t cand_key[256];
+  double cand_ratio[256];
+  double cand_t[256];
   uint32_t ticket;
   uint32_t cap_ok;       // 1: passes >= 1 and the selection run on the compacted entries (see k_count)
   uint32_t cmp_key;      // key above which the first count pass compacts elements
@@ -54,6 +53,9 @@ struct Ctrl {
   double thres_log[NMAX];
   uint32_t key_log[NMAX];
   uint32_t nnz_log[NMAX];
+  uint64_t phase_ns[8];  // %globaltimer at the phase boundaries of the last k_compress (CTA 0)
+  uint32_t n_phase;
+  uint32_t n_compacted;  // entries kept by the first count pass (all warps)
 };
 
 // Per-launch parameters of the MSTopK kernels.  The count and selection kernels share one
@@ -105,19 +107,20 @@ __device__ __forceinline__ uint32_t key_of(double t) {
 // Candidates of one count pass: the 2^lev - 1 ratios of the next lev bisection levels below the
 // current [lo, hi], ascending.  Every ratio is dyadic with <= 52 significant bits, so
 // lo + (hi-lo)*m/2^lev is exact and equals the sequential l + (r-l)/2 of Alg. 1 l.8 (Q5).
-__device__ void make_candidates(Ctrl* c, int lev) {
-  const int T = (1 << lev) - 1;
-  const double w = __dsub_rn(c->hi, c->lo);
-  const double inv = ldexp(1.0, -lev);
-  for (int m = 1; m <= T; ++m) {
-    const double ratio = __dadd_rn(c->lo, __dmul_rn(w, (double)m * inv));
+// Computed by the CTA's threads in parallel (candidate m-1 by thread m-1); the caller
+// synchronises the CTA before and after.
+__device__ void make_candidates_par(Ctrl* c, int lev) {
+  const int T = (1 << lev) - 1;  // <= 255: one candidate per thread
+  const int m = (int)threadIdx.x + 1;
+  if (m <= T) {
+    const double w = __dsub_rn(c->hi, c->lo);
+    const double ratio = __dadd_rn(c->lo, __dmul_rn(w, (double)m * ldexp(1.0, -lev)));
     const double t = threshold_of(c->abar, c->U, ratio);
     c->cand_ratio[m - 1] = ratio;
     c->cand_t[m - 1] = t;
     c->cand_key[m - 1] = key_of(t);
-    c->totals[m - 1] = 0u;
   }
-  c->ncand = (uint32_t)T;
+  if (threadIdx.x == 0) c->ncand = (uint32_t)T;
 }
 
 // Replay lev levels of Alg. 1 l.8-23 on the candidates' exact counts.
@@ -255,14 +258,7 @@ __device__ void stats_finalize(Ctrl* c, const SearchParams& sp, double S, uint32
   c->prov1 = -1; c->prov2 = -1;
   c->it = 0u;
   c->step = step;
-  make_candidates(c, first_levels);
-  // compaction key of the first count pass: the highest of its candidates at or below the
-  // bracket the previous compression ended in (any choice is exact; a good one keeps few elements)
-  int ms = 0;
-  for (int q = 1; q < (int)c->ncand; ++q)
-    if (c->cand_ratio[q] <= c->prev_lo) ms = q;
-  c->cmp_key = c->cand_key[ms];
-  c->cmp_ratio = c->cand_ratio[ms];
+  (void)first_levels;
 }
 
 // HiTopKComm step 1 fused into K1 (Eq. 4; reading Q20): with NP > 0 the gradient of
@@ -316,10 +312,9 @@ __device__ __forceinline__ void ef_load(const float* g, const Peers& pr, const f
 }
 
 template <bool EF, int NP>
-__global__ void __launch_bounds__(THREADS, 4) k_ef_stats(const float* __restrict__ g, Peers pr, float* __restrict__ r,
-                                                         SearchParams sp, uint32_t units_per_warp,
-                                                         double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max,
-                                                         Ctrl* __restrict__ c, uint64_t step, int first_levels) {
+__device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peers& pr, float* __restrict__ r,
+                                         const SearchParams& sp, uint32_t units_per_warp,
+                                         double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max) {
   __shared__ double s_ws[WARPS];
   __shared__ uint32_t s_wm[WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -392,11 +387,16 @@ __global__ void __launch_bounds__(THREADS, 4) k_ef_stats(const float* __restrict
     for (int w = 1; w < WARPS; ++w) m = max(m, s_wm[w]);
     cta_max[blockIdx.x] = m;
   }
-  if (!last_cta(&c->ticket)) return;
-  // ---- last CTA: canonical tree over the CTA partials, zero-padded to Lp = 2^j >= THREADS ----
+}
+
+// Root of the canonical tree (every CTA computes it, identically, after the grid barrier):
+// the CTA partials zero-padded to Lp = 2^j >= THREADS leaves (extra zero leaves never change a
+// pairwise sum of non-negatives, Q3), then a-bar, u and the first pass's candidates.
+__device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* __restrict__ cta_max,
+                           const SearchParams& sp, Ctrl* sc, uint64_t step, int first_levels) {
   __shared__ double s_v[THREADS];
   __shared__ uint32_t s_m[WARPS];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t Lp = THREADS;
   while (Lp < gridDim.x) Lp <<= 1;
   const uint32_t G = Lp / THREADS;  // <= 8 for grids up to 2048 CTAs
@@ -434,209 +434,90 @@ __global__ void __launch_bounds__(THREADS, 4) k_ef_stats(const float* __restrict
     if (tid < h) s_v[tid] = v;
     __syncthreads();
   }
-  __shared__ Ctrl sc;
-  ctrl_to_smem(&sc, c);
   if (tid == 0) {
     uint32_t m = s_m[0];
     for (int w = 1; w < WARPS; ++w) m = max(m, s_m[w]);
-    sc.ticket = 0u;
-    stats_finalize(&sc, sp, s_v[0], m, step, first_levels);
+    stats_finalize(sc, sp, s_v[0], m, step, first_levels);
   }
-  ctrl_to_global(c, &sc);
+  __syncthreads();
+  make_candidates_par(sc, first_levels);
+  __syncthreads();
+  if (tid == 0) {
+    // compaction key of the first count pass: the highest of its candidates at or below the
+    // bracket the previous compression ended in (any choice is exact; a good one keeps few elements)
+    int ms = 0;
+    for (int q = 1; q < (int)sc->ncand; ++q)
+      if (sc->cand_ratio[q] <= sc->prev_lo) ms = q;
+    sc->cmp_key = sc->cand_key[ms];
+    sc->cmp_ratio = sc->cand_ratio[ms];
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------------------------------
-// K2: count pass (Alg. 1 l.10) resolving LEV bisection levels per read of the data: the
-// T = 2^LEV - 1 candidate keys are sorted, so each element's bucket b = #{s : key_s <= bits}
-// is found by a LEV-step binary search, and buckets are counted in packed 8-bit fields of a
-// 64-bit register (flushed every 15 rounds).  nnz_s = sum_{b > s} bucket_b exactly.
-// Per-warp-slab counts are kept (the selection's prefix sums reuse them); the last CTA replays
-// the LEV levels of Alg. 1 l.11-23 and emits the next candidates, or after the last pass
-// computes the window (l.27) and the slab prefix sums of the two selection classes.
-// HBM/L2: 4 B/elem.
-template <int LEV>
-__device__ __forceinline__ uint32_t bucket_of(int32_t a, int32_t root, const int32_t* s_key) {
-  uint32_t b = (a >= root) ? (1u << (LEV - 1)) : 0u;
-#pragma unroll
-  for (int l = LEV - 2; l >= 0; --l) {
-    const int32_t kk = s_key[b + (1u << l) - 1];
-    b += (a >= kk) ? (1u << l) : 0u;
-  }
-  return b;
-}
+// Count passes (Alg. 1 l.10): one read of the data resolves LEV bisection levels at once - the
+// T = 2^LEV - 1 candidate thresholds of those levels are counted together (integer keys, Q4) and
+// Alg. 1 l.11-23 is replayed on the exact totals.  Three modes:
+//   COUNT_FIRST   whole vector, LEV <= 2; also appends, per warp and in index order, every element
+//                 at or above the compaction key (one of the candidate keys) to the warp's entries
+//   COUNT_CAP     the warp's compacted entries only (exact when the bracket lies above the key), LEV <= 4
+//   COUNT_FULL    whole vector, LEV <= 2 (the general path when the compacted one is not exact)
+// Each element costs one compare-and-add per key.  Per-warp-slab counts are stored (wcnt) for the
+// selection's prefix sums; per-CTA sums go to the pass's global totals.
+// HBM/L2: 4 B/elem (FIRST, FULL), 4 B/entry (CAP); FIRST also writes 8 B per compacted entry.
+enum { COUNT_FIRST = 0, COUNT_CAP = 1, COUNT_FULL = 2 };
 
-// Exclusive prefix over the W warp slabs of the class-1 (a >= thres1) and class-2
-// (thres2 <= a < thres1) counts, taken from the per-slab counts of the trials that set thres1 /
-// thres2.  Chunks of 8*THREADS slabs are staged through shared memory with coalesced loads.
-__device__ __noinline__ void scan_slabs(const Ctrl* c, const SearchParams& sp, const uint32_t* __restrict__ wcnt,
-                                        uint32_t* __restrict__ pre1, uint32_t* __restrict__ pre2) {
-  constexpr int PER = 8;
-  constexpr int CH = PER * THREADS;
-  __shared__ uint32_t s_c1[CH], s_ca[CH];
-  __shared__ uint32_t s_w[2][WARPS];
-  const int32_t p1 = c->prov1, p2 = c->prov2;
-  const uint32_t W = sp.W;
-  uint32_t carry1 = 0, carry2 = 0;
-  for (uint32_t c0 = 0; c0 < W; c0 += CH) {
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const uint32_t w = c0 + i * THREADS + threadIdx.x;
-      uint32_t x1 = 0u, xa = 0u;
-      if (w < W) {
-        if (p1 >= 0) x1 = __ldcg(wcnt + (size_t)p1 * W + w);
-        if (p2 >= 0) {
-          xa = __ldcg(wcnt + (size_t)p2 * W + w);
-        } else {
-          const uint64_t lo = min(sp.n, (uint64_t)w * sp.S);
-          xa = (uint32_t)(min(sp.n, lo + sp.S) - lo);
-        }
-      }
-      s_c1[i * THREADS + threadIdx.x] = x1;
-      s_ca[i * THREADS + threadIdx.x] = xa;
-    }
-    __syncthreads();
-    uint32_t a1 = 0, a2 = 0;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const uint32_t x1 = s_c1[threadIdx.x * PER + i];
-      a1 += x1;
-      a2 += s_ca[threadIdx.x * PER + i] - x1;
-    }
-    uint32_t t1, t2;
-    uint32_t r1 = carry1 + block_excl_scan(a1, s_w[0], t1);
-    uint32_t r2 = carry2 + block_excl_scan(a2, s_w[1], t2);
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const uint32_t w = c0 + threadIdx.x * PER + i;
-      const uint32_t x1 = s_c1[threadIdx.x * PER + i];
-      const uint32_t x2 = s_ca[threadIdx.x * PER + i] - x1;
-      if (w < W) {
-        pre1[w] = r1;
-        pre2[w] = r2;
-      }
-      r1 += x1;
-      r2 += x2;
-    }
-    carry1 += t1;
-    carry2 += t2;
-    __syncthreads();
-  }
-}
-
-template <int LEV, bool FIRST>
-__global__ void __launch_bounds__(THREADS, 3) k_count(const float* __restrict__ acc, Ctrl* __restrict__ c,
-                                                      SearchParams sp, uint32_t* __restrict__ wcnt,
-                                                      uint32_t* __restrict__ pre1, uint32_t* __restrict__ pre2,
-                                                      Compact cp, int pass, int next_lev) {
+template <int LEV, int MODE>
+__device__ __forceinline__ void count_phase(const float* __restrict__ acc, const Ctrl* sc, const SearchParams sp,
+                                            uint32_t* __restrict__ wcnt, const Compact cp, uint32_t* totals,
+                                            uint32_t* overflow, int pass) {
   constexpr int T = (1 << LEV) - 1;
-  constexpr int NB = 1 << LEV;  // buckets
-  // Full-vector mode: LEV <= 2 compares every element against the T keys directly
-  // (count_s += a >= key_s); LEV >= 3 gives the bucket search only to elements inside
-  // [key_0, key_{T-1}) (the others are below every key or counted in `above`).
-  // Compacted mode (passes >= 1 when c->cap_ok): direct compares over the warp's entries.
-  constexpr bool BRACKET = LEV >= 3;
-  __shared__ int32_t s_key[16];
-  __shared__ uint32_t s_cnt[WARPS][T];
-  __shared__ uint32_t s_bkt[WARPS][NB];  // per-warp bucket totals (flushed from packed registers)
+  __shared__ uint32_t s_cnt[WARPS][16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < T) s_key[threadIdx.x] = (int32_t)c->cand_key[threadIdx.x];
-  if (lane < NB) s_bkt[warp][lane] = 0u;
-  const bool cap_mode = !FIRST && c->cap_ok != 0u;
-  const int32_t kcmp = (int32_t)c->cmp_key;
-  __syncthreads();
-  int32_t kr[T], km1[T];  // keys and keys - 1 (a >= k  <=>  (k - 1 - a) < 0, no overflow for a, k >= 0)
+  int32_t km1[T];  // key - 1: a >= key  <=>  (key - 1 - a) < 0 (no overflow for 0 <= a, key < 2^31)
 #pragma unroll
-  for (int s = 0; s < T; ++s) {
-    kr[s] = s_key[s];
-    km1[s] = kr[s] - 1;
-  }
-  const int32_t root = kr[(1 << (LEV - 1)) - 1];
-  const int32_t kmin = kr[0], kmax = kr[T - 1];
-  const uint32_t width = (uint32_t)(kmax - kmin);
+  for (int s = 0; s < T; ++s) km1[s] = (int32_t)sc->cand_key[s] - 1;
+  const int32_t kcmp1 = (int32_t)sc->cmp_key - 1;
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint64_t lo = min(sp.n, (uint64_t)gw * sp.S);
   const uint64_t hi = min(sp.n, lo + sp.S);
   const uint32_t* a32 = reinterpret_cast<const uint32_t*>(acc);
-  uint32_t direct[T];  // count_s (direct mode)
-  uint32_t ge[T];      // this warp's nnz per candidate
-  uint32_t above = 0;
-  uint64_t pk0 = 0, pk1 = 0;  // packed 8-bit bucket counters of in-bracket elements (buckets 0-7, 8-15)
-  int since_flush = 0;
-  uint32_t ncomp = 0;         // FIRST: compacted entries of this warp so far
-  auto flush = [&]() {
+  uint32_t cnt[T];
 #pragma unroll
-    for (int b = 1; b < NB; ++b) {
-      const uint64_t w = (b < 8) ? pk0 : pk1;
-      const uint32_t t = __reduce_add_sync(0xffffffffu, (uint32_t)((w >> (8 * (b & 7))) & 0xFFu));
-      if (lane == 0) s_bkt[warp][b] += t;
-    }
-    pk0 = 0;
-    pk1 = 0;
-    since_flush = 0;
-  };
-  auto add_bucket = [&](int32_t a) {
-    const uint32_t b = bucket_of<LEV>(a, root, s_key);
-    if (LEV <= 3) {
-      pk0 += 1ull << (8 * b);
-    } else {
-      const uint64_t inc = 1ull << (8 * (b & 7));
-      if (b & 8) pk1 += inc; else pk0 += inc;
-    }
-  };
-  auto direct_one = [&](uint32_t bits) {
+  for (int s = 0; s < T; ++s) cnt[s] = 0;
+  auto count1 = [&](uint32_t bits) {
     const int32_t a = (int32_t)(bits & 0x7FFFFFFFu);
 #pragma unroll
-    for (int s = 0; s < T; ++s) direct[s] += (uint32_t)(km1[s] - a) >> 31;  // IADD3 + LEA.HI
+    for (int s = 0; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
   };
-
-  if (cap_mode) {
-    // ---- compacted entries of this warp: direct compares ----
-#pragma unroll
-    for (int s = 0; s < T; ++s) direct[s] = 0;
+  if (MODE == COUNT_CAP) {
     const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
     const uint32_t* eb = cp.bits + (size_t)gw * cp.C;
-    for (uint32_t j0 = 0; j0 < ne; j0 += 128) {
-      const uint32_t j = j0 + 4 * lane;
-      if (j + 4 <= ne) {
-        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(eb + j));
-        direct_one(q.x); direct_one(q.y); direct_one(q.z); direct_one(q.w);
-      } else {
-        for (uint32_t t = j; t < ne && t < j + 4; ++t) direct_one(__ldcg(eb + t));
-      }
-    }
+    // this warp's entry loads in flight together (4 x 128 entries per iteration)
+    for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
+      uint4 q[4];
 #pragma unroll
-    for (int s = 0; s < T; ++s) ge[s] = __reduce_add_sync(0xffffffffu, direct[s]);
-  } else {
-    if (!BRACKET) {
-#pragma unroll
-      for (int s = 0; s < T; ++s) direct[s] = 0;
-    }
-    // ---- whole slab ----
-    auto one = [&](uint32_t bits, uint32_t& inb, int j) {
-      const int32_t a = (int32_t)(bits & 0x7FFFFFFFu);
-      if (!BRACKET) {
-        direct_one(bits);
-      } else {
-        above += (a >= kmax) ? 1u : 0u;
-        inb |= ((uint32_t)(a - kmin) < width) ? (1u << j) : 0u;
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u * 128 + 4 * lane;
+        q[u] = make_uint4(0u, 0u, 0u, 0u);
+        if (j + 4 <= ne) q[u] = __ldcg(reinterpret_cast<const uint4*>(eb + j));
       }
-    };
-    // rare path: bucket search for the in-bracket elements of a round (re-read through L1/L2 by
-    // index, so the round's registers need not stay live)
-    auto slow = [&](uint64_t rbase, uint32_t inb) {
-      if (BRACKET && __any_sync(0xffffffffu, inb != 0u)) {
-#pragma unroll 1
-        for (uint32_t m = inb; m; m &= m - 1u) {
-          const int j = __ffs(m) - 1;
-          const uint32_t bits = __ldg(a32 + rbase + 4 * lane + (j >> 2) * 128 + (j & 3));
-          add_bucket((int32_t)(bits & 0x7FFFFFFFu));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u * 128 + 4 * lane;
+        if (j + 4 <= ne) {
+          count1(q[u].x); count1(q[u].y); count1(q[u].z); count1(q[u].w);
+        } else {
+          for (uint32_t t = j; t < ne && t < j + 4; ++t) count1(__ldcg(eb + t));
         }
       }
-    };
-    // FIRST: append the round's elements >= the compaction key to the warp's entries, in index
-    // order (chunk, lane, element); one packed warp scan covers the four chunks
-    const int32_t kcmp1 = kcmp - 1;
-    auto compact = [&](const uint4* v, uint64_t rbase, uint32_t valid) {
+    }
+  } else {
+    uint32_t ncomp = 0;  // FIRST: entries appended by this warp so far
+    // FIRST: append the round's elements >= the compaction key in index order (chunk, lane,
+    // element); one packed warp scan covers the four chunks
+    auto compact = [&](uint4 v0, uint4 v1, uint4 v2, uint4 v3, uint64_t rbase, uint32_t valid) {
+      const uint4 v[4] = {v0, v1, v2, v3};
       uint32_t m = 0;
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
@@ -647,8 +528,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_count(const float* __restrict__ 
       }
       m &= valid;
       if (!__any_sync(0xffffffffu, m != 0u)) return;
-      // per-chunk counts of this lane (<= 4 each) packed in bytes; warp sums stay <= 128
-      uint32_t packed = 0;
+      uint32_t packed = 0;  // per-chunk counts of this lane (<= 4) in bytes; warp sums <= 128
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) packed |= (uint32_t)__popc((m >> (4 * ch)) & 0xFu) << (8 * ch);
       uint32_t incl = packed;
@@ -682,82 +562,67 @@ __global__ void __launch_bounds__(THREADS, 3) k_count(const float* __restrict__ 
       }
       ncomp = chunk_base;
     };
-    auto consume = [&](const uint4* v, uint64_t rbase) {
-      uint32_t inb = 0;
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        one(v[ch].x, inb, 4 * ch);
-        one(v[ch].y, inb, 4 * ch + 1);
-        one(v[ch].z, inb, 4 * ch + 2);
-        one(v[ch].w, inb, 4 * ch + 3);
-      }
-      slow(rbase, inb);
-      if (FIRST) compact(v, rbase, 0xFFFFu);
-      if (BRACKET && ++since_flush == 15) flush();
-    };
-    // software pipeline, two rounds deep: while round i is counted, the 128-bit loads of rounds
-    // i+1 and i+2 are in flight (8 per lane)
-    uint4 va[4], vb[4];
-    auto load_round = [&](uint64_t b, uint4* dst) {
-      const uint64_t e0 = b + 4 * lane;
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) dst[ch] = *reinterpret_cast<const uint4*>(a32 + e0 + ch * 128);
-    };
+    // two rounds of 128-bit loads in flight per lane while a round is counted
+    const uint64_t e0 = lo + 4 * lane;
     const uint64_t nfull = (hi - lo) / ROUND;  // full rounds of this slab
-    uint64_t base = lo;
-    if (nfull > 0) load_round(base, va);
-    if (nfull > 1) load_round(base + ROUND, vb);
+    uint4 a0 = make_uint4(0u, 0u, 0u, 0u), a1 = a0, a2 = a0, a3 = a0, b0 = a0, b1 = a0, b2 = a0, b3 = a0;
+#define TK_LOAD(q0, q1, q2, q3, r)                                              \
+  do {                                                                        \
+    const uint4* p_ = reinterpret_cast<const uint4*>(a32 + e0 + (r) * ROUND); \
+    q0 = p_[0];                                                               \
+    q1 = p_[32];                                                              \
+    q2 = p_[64];                                                              \
+    q3 = p_[96];                                                              \
+  } while (0)
+#define TK_COUNT(q0, q1, q2, q3, r)                                                 \
+  do {                                                                            \
+    count1(q0.x); count1(q0.y); count1(q0.z); count1(q0.w);                       \
+    count1(q1.x); count1(q1.y); count1(q1.z); count1(q1.w);                       \
+    count1(q2.x); count1(q2.y); count1(q2.z); count1(q2.w);                       \
+    count1(q3.x); count1(q3.y); count1(q3.z); count1(q3.w);                       \
+    if (MODE == COUNT_FIRST) compact(q0, q1, q2, q3, lo + (r) * ROUND, 0xFFFFu); \
+  } while (0)
+    if (nfull > 0) TK_LOAD(a0, a1, a2, a3, 0);
+    if (nfull > 1) TK_LOAD(b0, b1, b2, b3, 1);
     for (uint64_t i = 0; i < nfull; i += 2) {
-      consume(va, base);
-      if (i + 2 < nfull) load_round(base + 2 * ROUND, va);
+      TK_COUNT(a0, a1, a2, a3, i);
+      if (i + 2 < nfull) TK_LOAD(a0, a1, a2, a3, i + 2);
       if (i + 1 < nfull) {
-        consume(vb, base + ROUND);
-        if (i + 3 < nfull) load_round(base + 3 * ROUND, vb);
+        TK_COUNT(b0, b1, b2, b3, i + 1);
+        if (i + 3 < nfull) TK_LOAD(b0, b1, b2, b3, i + 3);
       }
-      base += 2 * ROUND;
     }
-    base = lo + nfull * ROUND;
+#undef TK_LOAD
+#undef TK_COUNT
+    const uint64_t base = lo + nfull * ROUND;
     if (base < hi) {  // ragged tail round (end of the vector only)
-      const uint64_t e0 = base + 4 * lane;
-      uint32_t inb = 0, valid = 0;
-      uint4 v[4];
+      uint32_t w[16], valid = 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const uint64_t i = e0 + (j >> 2) * 128 + (j & 3);
-        const uint32_t bits = (i < hi) ? a32[i] : 0u;
+        const uint64_t i = base + 4 * lane + (j >> 2) * 128 + (j & 3);
+        w[j] = 0u;
         if (i < hi) {
-          one(bits, inb, j);
+          w[j] = a32[i];
+          count1(w[j]);
           valid |= 1u << j;
         }
-        uint32_t* vj = reinterpret_cast<uint32_t*>(&v[j >> 2]) + (j & 3);
-        *vj = bits;
       }
-      slow(base, inb);
-      if (FIRST) compact(v, base, valid);
+      if (MODE == COUNT_FIRST)
+        compact(make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]),
+                make_uint4(w[8], w[9], w[10], w[11]), make_uint4(w[12], w[13], w[14], w[15]), base, valid);
     }
-    if (BRACKET) flush();
-    if (FIRST && lane == 0) {
+    if (MODE == COUNT_FIRST && lane == 0) {
       cp.cnt[gw] = ncomp;
-      if (ncomp > cp.C) atomicOr(&c->overflow, 1u);
-    }
-    __syncwarp();
-    if (BRACKET) {
-      uint32_t run = __reduce_add_sync(0xffffffffu, above);
-#pragma unroll
-      for (int b = NB - 1; b >= 1; --b) {
-        run += s_bkt[warp][b];
-        ge[b - 1] = run;
-      }
-    } else {
-#pragma unroll
-      for (int s = 0; s < T; ++s) ge[s] = __reduce_add_sync(0xffffffffu, direct[s]);
+      if (ncomp > cp.C) atomicOr(overflow, 1u);
     }
   }
-  if (lane == 0) {
+  // warp totals -> per-slab counts and the CTA's contribution to the pass totals
 #pragma unroll
-    for (int s = 0; s < T; ++s) {
-      wcnt[(size_t)(pass * TMAX + s) * sp.W + gw] = ge[s];
-      s_cnt[warp][s] = ge[s];
+  for (int s = 0; s < T; ++s) {
+    const uint32_t t = __reduce_add_sync(0xffffffffu, cnt[s]);
+    if (lane == 0) {
+      wcnt[(size_t)(pass * TMAX + s) * sp.W + gw] = t;
+      s_cnt[warp][s] = t;
     }
   }
   __syncthreads();
@@ -765,28 +630,82 @@ __global__ void __launch_bounds__(THREADS, 3) k_count(const float* __restrict__ 
     uint32_t tot = 0;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) tot += s_cnt[w][threadIdx.x];
-    atomicAdd(&c->totals[threadIdx.x], tot);
-  }
-  if (!last_cta(&c->ticket)) return;
-  __shared__ uint32_t s_tot[16];
-  __shared__ Ctrl sc;
-  if (threadIdx.x < T) s_tot[threadIdx.x] = __ldcg(&c->totals[threadIdx.x]);
-  ctrl_to_smem(&sc, c);
-  if (threadIdx.x == 0) {
-    const double lo_key_ratio = sc.cmp_ratio;
-    replay_levels(&sc, s_tot, LEV, pass, sp.k);
-    sc.ticket = 0u;
-    if (FIRST) {
-      // compacted mode is exact iff every later threshold (and thres2) lies above the compaction
-      // key: the bracket's lower end must have reached its ratio, and nothing overflowed
-      sc.cap_ok = (sc.lo >= lo_key_ratio && sc.overflow == 0u) ? 1u : 0u;
-      sc.overflow = 0u;
-    }
-    if (next_lev > 0) make_candidates(&sc, next_lev); else finish_window(&sc, sp);
+    atomicAdd(&totals[threadIdx.x], tot);
   }
   __syncthreads();
-  if (next_lev == 0) scan_slabs(&sc, sp, wcnt, pre1, pre2);
-  ctrl_to_global(c, &sc);
+}
+
+// COUNT_HIST (compacted entries, up to HIST_LEV levels in ONE pass): the T = 2^LEV - 1 sorted
+// candidate keys sit in shared memory; each entry finds its bucket b = #{s : key_s <= a} by a
+// LEV-step binary search and bumps a per-warp shared-memory histogram; the CTA histogram is added
+// to the pass's global histogram; after the barrier nnz_s = sum_{b > s} hist[b] (exact).
+constexpr int HIST_LEV = 8;
+constexpr int HIST_BINS = 1 << HIST_LEV;
+
+struct HistSmem {
+  int32_t key[HIST_BINS];
+  uint32_t h[WARPS][HIST_BINS];
+};
+
+template <int LEV>
+__device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uint32_t* ghist, HistSmem& hs) {
+  constexpr int T = (1 << LEV) - 1;
+  constexpr int NB = 1 << LEV;
+  int32_t* s_key = hs.key;
+  auto& s_h = hs.h;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < T; i += THREADS) s_key[i] = (int32_t)sc->cand_key[i];
+  for (int i = lane; i < NB; i += 32) s_h[warp][i] = 0u;
+  __syncthreads();
+  const uint32_t gw = blockIdx.x * WARPS + warp;
+  const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
+  const uint32_t* eb = cp.bits + (size_t)gw * cp.C;
+  auto add = [&](uint32_t bits) {
+    const int32_t a = (int32_t)(bits & 0x7FFFFFFFu);
+    uint32_t b = 0;
+#pragma unroll
+    for (int l = LEV - 1; l >= 0; --l) b += (a >= s_key[b + (1u << l) - 1]) ? (1u << l) : 0u;
+    atomicAdd(&s_h[warp][b], 1u);
+  };
+  for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
+    uint4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t j = j0 + u * 128 + 4 * lane;
+      q[u] = make_uint4(0u, 0u, 0u, 0u);
+      if (j + 4 <= ne) q[u] = __ldcg(reinterpret_cast<const uint4*>(eb + j));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t j = j0 + u * 128 + 4 * lane;
+      if (j + 4 <= ne) {
+        add(q[u].x); add(q[u].y); add(q[u].z); add(q[u].w);
+      } else {
+        for (uint32_t t = j; t < ne && t < j + 4; ++t) add(__ldcg(eb + t));
+      }
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < NB; b += THREADS) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) t += s_h[w][b];
+    if (b > 0 && t) atomicAdd(ghist + b, t);  // bucket 0 (below every key) is never needed
+  }
+  __syncthreads();
+}
+
+// nnz of every candidate from the global histogram: nnz_s = sum_{b >= s+1} hist[b]
+__device__ __forceinline__ void hist_to_counts(const uint32_t* ghist, int lev, uint32_t* s_tot) {
+  __shared__ uint32_t s_w[WARPS];
+  const int NB = 1 << lev;
+  // thread t owns bin NB-1-t (a reversed inclusive scan gives the suffix sums)
+  const int b = NB - 1 - (int)threadIdx.x;
+  const uint32_t v = (b >= 1) ? __ldcg(ghist + b) : 0u;
+  uint32_t total;
+  const uint32_t excl = block_excl_scan(v, s_w, total);
+  if (b >= 1) s_tot[b - 1] = excl + v;  // sum over bins b..NB-1 = nnz of candidate b-1
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -798,11 +717,10 @@ __global__ void __launch_bounds__(THREADS, 3) k_count(const float* __restrict__ 
 // slab's exclusive prefix counts; rounds without any class-1/2 element cost a ballot only, and a
 // slab that provably holds no kept element is not read at all.
 // HBM/L2: <= 4 B/elem read + 8 B per selected pair + a 4-byte residual zero per selected pair.
-__global__ void __launch_bounds__(THREADS, 3) k_select(const float* __restrict__ acc, const Ctrl* __restrict__ c,
-                                                       SearchParams sp, const uint32_t* __restrict__ wcnt,
-                                                       const uint32_t* __restrict__ pre1, const uint32_t* __restrict__ pre2,
-                                                       uint32_t* __restrict__ idx_out, float* __restrict__ val_out,
-                                                       float* __restrict__ r_zero, Compact cp) {
+__device__ __forceinline__ void select_phase(const float* __restrict__ acc, const Ctrl* c, const SearchParams sp,
+                                          uint32_t c1, uint32_t c2, uint32_t b1, uint32_t b2,
+                                          uint32_t* __restrict__ idx_out, float* __restrict__ val_out,
+                                          float* __restrict__ r_zero, const Compact cp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint64_t lo = min(sp.n, (uint64_t)gw * sp.S);
@@ -812,17 +730,11 @@ __global__ void __launch_bounds__(THREADS, 3) k_select(const float* __restrict__
   const int32_t key1 = (p1 >= 0) ? (int32_t)c->key1 : (int32_t)INF_BITS;
   const int32_t key2 = (p2 >= 0) ? (int32_t)c->key2 : 0;
   const uint32_t rnd = (uint32_t)c->rand, need = c->need;
-  uint32_t b1 = pre1[gw], b2 = pre2[gw];
-  {
-    const uint32_t c1 = p1 >= 0 ? wcnt[(size_t)p1 * sp.W + gw] : 0u;
-    const uint32_t call = p2 >= 0 ? wcnt[(size_t)p2 * sp.W + gw] : (uint32_t)(hi - lo);
-    const uint32_t c2 = call - c1;
-    if (c1 == 0 && (c2 == 0 || b2 >= rnd + need || b2 + c2 <= rnd)) return;  // nothing kept here
-  }
+  if (c1 == 0 && (c2 == 0 || b2 >= rnd + need || b2 + c2 <= rnd)) return;  // nothing kept here
   if (c->cap_ok) {
     // ---- compacted entries of this warp (ascending index order): 128 per iteration, lane l
     // holds entries 4l..4l+3 of the group, so (lane, e) order is index order ----
-    const uint32_t ne = min(cp.cnt[gw], cp.C);
+    const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
     const uint32_t* ei = cp.idx + (size_t)gw * cp.C;
     const uint32_t* eb = cp.bits + (size_t)gw * cp.C;
     for (uint32_t j0 = 0; j0 < ne; j0 += 128) {
@@ -976,6 +888,214 @@ __global__ void __launch_bounds__(THREADS, 3) k_select(const float* __restrict__
     }
     if (__any_sync(0xffffffffu, cand != 0u)) emit(base, cand);
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// The whole compression (A1-A8) as ONE persistent cooperative kernel: the phases above, separated
+// by grid barriers.  After each barrier every CTA runs the scalar control of Alg. 1 itself, on
+// its own shared-memory copy of the control block, from the same global totals - so every CTA
+// takes the same decisions and no serial tail, ticket or extra launch is needed.
+
+struct Fused {
+  SearchParams sp;
+  const float* g;            // gradient (flat) - unused when the peers supply it
+  Peers pr;                  // HiTopKComm ordered reduce-scatter sources
+  float* r;                  // residual in, acc / r' out (EF); nullptr without EF
+  const float* acc;          // the vector MSTopK reads: r (EF) or g
+  uint32_t units_per_warp;   // ef phase: aligned power-of-two run of 512-element units per warp
+  double* cta_sum;           // [grid] ef partials
+  uint32_t* cta_max;         // [grid]
+  uint32_t* wcnt;            // [npass * TMAX][W] per-warp-slab trial counts
+  uint32_t* totals;          // [npass][16] global trial counts
+  uint32_t* cta_cls;         // [2][grid] per-CTA class-1 / class-2 counts
+  uint32_t* bar;             // grid barrier: [0] arrivals, [1] generation
+  uint32_t* flags;           // [0] compaction overflow
+  Compact cp;
+  uint32_t* idx_out;
+  float* val_out;
+  Ctrl* c;                   // the control block (stats / next call's bracket prediction)
+  uint64_t step;
+  uint32_t n_iters;          // N
+  int lev0;                  // levels of the first (whole-vector) pass: min(2, N, cap_levels)
+  int cap_levels;            // max levels per later pass on compacted entries (whole-vector: <= 2)
+  int max_pass;              // passes for which totals / wcnt are allocated
+};
+
+// Grid-wide barrier (the launch is cooperative: every CTA is resident).  Arrivals are counted
+// on bar[0]; the last arrival resets it and bumps the generation bar[1] the others wait on.
+__device__ __forceinline__ void grid_sync(uint32_t* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile uint32_t* gen = bar + 1;
+    const uint32_t g0 = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g0) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int LEV, int MODE>
+__device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass) {
+  count_phase<LEV, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * pass, f.flags, pass);
+}
+
+template <bool EF, int NP>
+__global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
+  __shared__ Ctrl sc;
+  __shared__ uint32_t s_tot[HIST_BINS];
+  __shared__ HistSmem s_hist;
+  __shared__ uint32_t s_w[2][WARPS];
+  __shared__ uint32_t s_base[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)
+  int nph = 0;
+  auto stamp = [&]() {
+    if (tid == 0 && nph < 8) sc.phase_ns[nph] = globaltimer();
+    ++nph;
+    sc.n_phase = (uint32_t)min(nph, 8);
+  };
+  stamp();
+  if (blockIdx.x == 0) {
+    for (int i = tid; i < HIST_BINS * f.max_pass; i += THREADS) f.totals[i] = 0u;
+    if (tid == 0) f.flags[0] = 0u;
+  }
+  // ---- A1-A2: error feedback, |acc| pairwise tree and max ----
+  ef_phase<EF, NP>(f.g, f.pr, f.r, f.sp, f.units_per_warp, f.cta_sum, f.cta_max);
+  grid_sync(f.bar);
+  stamp();
+  stats_root(f.cta_sum, f.cta_max, f.sp, &sc, f.step, f.lev0);
+  // ---- A3-A5: count passes.  The first resolves lev0 levels on the whole vector and compacts;
+  // when the compacted entries are exact for the rest, each further pass resolves up to HIST_LEV
+  // levels on them at once (histogram pass), else up to 2 levels per pass on the whole vector.
+  // The bits do not depend on this schedule. ----
+  const int N = (int)f.n_iters;
+  int done = 0;
+  for (int p = 0; done < N; ++p) {
+    int lev;
+    bool hist = false;
+    uint32_t* tot_p = f.totals + HIST_BINS * p;
+    if (p == 0) {
+      lev = f.lev0;
+      if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, 0); else run_count<2, COUNT_FIRST>(f, &sc, 0);
+    } else if (sc.cap_ok) {
+      hist = true;
+      lev = min(min(HIST_LEV, f.cap_levels), N - done);
+      switch (lev) {
+        case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist); break;
+        case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist); break;
+        case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist); break;
+        case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist); break;
+        case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist); break;
+        case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist); break;
+        case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist); break;
+        default: hist_phase<8>(&sc, f.cp, tot_p, s_hist); break;
+      }
+    } else {
+      lev = min(min(2, f.cap_levels), N - done);
+      if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<2, COUNT_FULL>(f, &sc, p);
+    }
+    done += lev;
+    grid_sync(f.bar);
+    stamp();
+    if (hist) {
+      hist_to_counts(tot_p, lev, s_tot);
+    } else {
+      if (tid < 16) s_tot[tid] = __ldcg(tot_p + tid);
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const double cmp_ratio = sc.cmp_ratio;
+      replay_levels(&sc, s_tot, lev, p, f.sp.k);
+      if (p == 0) {
+        // compacted mode is exact iff every later threshold (and thres2) lies above the compaction
+        // key: the bracket's lower end must have reached its ratio, and nothing overflowed
+        sc.cap_ok = (sc.lo >= cmp_ratio && __ldcg(f.flags) == 0u) ? 1u : 0u;
+      }
+      if (done == N) finish_window(&sc, f.sp);
+    }
+    __syncthreads();
+    if (done < N) {
+      const int next = sc.cap_ok ? min(min(HIST_LEV, f.cap_levels), N - done) : min(min(2, f.cap_levels), N - done);
+      make_candidates_par(&sc, next);
+      __syncthreads();
+    }
+  }
+  // ---- A7 prefix: class-1 / class-2 counts of each warp slab, then of the CTAs before it ----
+  const uint32_t gw = blockIdx.x * WARPS + warp;
+  const uint32_t W = f.sp.W;
+  const uint64_t slo = min(f.sp.n, (uint64_t)gw * f.sp.S);
+  const uint64_t shi = min(f.sp.n, slo + f.sp.S);
+  uint32_t c1 = 0, call = 0;
+  if (sc.cap_ok) {
+    // count the warp's compacted entries at key1 / key2 directly (exact: both keys lie at or
+    // above every element excluded from the entries)
+    const int32_t k1m1 = sc.prov1 >= 0 ? (int32_t)sc.key1 - 1 : 0x7FFFFFFF;
+    const int32_t k2m1 = (int32_t)sc.key2 - 1;
+    const uint32_t ne = min(__ldcg(f.cp.cnt + gw), f.cp.C);
+    const uint32_t* eb = f.cp.bits + (size_t)gw * f.cp.C;
+    for (uint32_t j = lane; j < ne; j += 32) {
+      const int32_t a = (int32_t)(__ldcg(eb + j) & 0x7FFFFFFFu);
+      c1 += (uint32_t)(k1m1 - a) >> 31;
+      call += (uint32_t)(k2m1 - a) >> 31;
+    }
+    c1 = __reduce_add_sync(0xffffffffu, c1);
+    call = __reduce_add_sync(0xffffffffu, call);
+  } else {
+    c1 = sc.prov1 >= 0 ? __ldcg(f.wcnt + (size_t)sc.prov1 * W + gw) : 0u;
+    call = sc.prov2 >= 0 ? __ldcg(f.wcnt + (size_t)sc.prov2 * W + gw) : (uint32_t)(shi - slo);
+  }
+  const uint32_t c2 = call - c1;
+  if (lane == 0) {
+    s_w[0][warp] = c1;
+    s_w[1][warp] = c2;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t t1 = 0, t2 = 0;
+    for (int w = 0; w < WARPS; ++w) { t1 += s_w[0][w]; t2 += s_w[1][w]; }
+    f.cta_cls[blockIdx.x] = t1;
+    f.cta_cls[gridDim.x + blockIdx.x] = t2;
+  }
+  grid_sync(f.bar);
+  stamp();
+  {
+    uint32_t a1 = 0, a2 = 0;
+    for (uint32_t b = tid; b < blockIdx.x; b += THREADS) {
+      a1 += __ldcg(f.cta_cls + b);
+      a2 += __ldcg(f.cta_cls + gridDim.x + b);
+    }
+    a1 = __reduce_add_sync(0xffffffffu, a1);
+    a2 = __reduce_add_sync(0xffffffffu, a2);
+    __shared__ uint32_t s_red[2][WARPS];
+    if (lane == 0) { s_red[0][warp] = a1; s_red[1][warp] = a2; }
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t b1 = 0, b2 = 0;
+      for (int w = 0; w < WARPS; ++w) { b1 += s_red[0][w]; b2 += s_red[1][w]; }
+      s_base[0] = b1;
+      s_base[1] = b2;
+    }
+    __syncthreads();
+  }
+  uint32_t b1 = s_base[0], b2 = s_base[1];
+  for (int w = 0; w < warp; ++w) { b1 += s_w[0][w]; b2 += s_w[1][w]; }
+  // ---- A7-A8: selection, compaction, residual write-back ----
+  select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, f.idx_out, f.val_out, EF ? f.r : nullptr, f.cp);
+  stamp();
+  if (blockIdx.x == 0) ctrl_to_global(f.c, &sc);
 }
 
 // ------------------------------------------------------------------------------------------

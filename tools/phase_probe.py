@@ -1,0 +1,25 @@
+"""Per-phase device time of k_compress in the bench regime (fresh N(0,1) gradients, EF from r=0)."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2010_10458_b200 as tk
+
+d = int(sys.argv[1]) if len(sys.argv) > 1 else 25_600_000
+steps = 60
+ctx = tk.Context(d, rho=0.001, n_iters=10, seed=1)
+gen = torch.Generator(device="cuda")
+gen.manual_seed(5)
+gs = [torch.randn(d, generator=gen, device="cuda") for _ in range(8)]
+r = torch.zeros(d, device="cuda")
+out = torch.empty(d, device="cuda")
+acc = None
+for s in range(steps):
+    ctx.step(gs[s % 8], r, out)
+    if s >= 20:
+        st = ctx.stats()
+        acc = st.phase_us if acc is None else [a + b for a, b in zip(acc, st.phase_us)]
+n = steps - 20
+names = ["ef+stats"] + [f"pass{i}" for i in range(len(acc) - 3)] + ["prefix", "select"]
+print("phases (us):", {names[i] if i < len(names) else i: round(v / n, 1) for i, v in enumerate(acc)},
+      "total", round(sum(acc) / n, 1), "compacted", st.compacted)
