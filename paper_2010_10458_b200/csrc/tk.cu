@@ -449,22 +449,22 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
   if (!aligned16(g) || !aligned16(out) || (ef && !aligned16(r))) return fail(c, TK_ERR_INVALID_ARG, "misaligned pointer");
   if ((const void*)g == (const void*)r || (const void*)g == (const void*)out || (const void*)r == (const void*)out)
     return fail(c, TK_ERR_INVALID_ARG, "g, r and out must not alias");
-  uint32_t* send = c->send;
-  const size_t kb = sizeof(uint32_t) * c->k;
   mark(c, TK_STAGE_NONE);
   if (c->n == 1) {
-    // flat NaiveAG: compress -> one packed all-gather -> rank-ordered decompress
-    TK_TRY(compress_impl(c, g, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k)));
+    // flat NaiveAG: compress straight into this rank's slot of the gathered buffer -> one packed
+    // in-place all-gather -> rank-ordered decompress
     uint32_t* gat = gathered ? gathered : c->recv;
-    if (c->P > 1) {
-      TK_NCCL(c, ncclAllGather(send, gat, 2 * c->k, ncclUint32, c->world, c->stream));
-    } else {
-      TK_CUDA(c, cudaMemcpyAsync(gat, send, 2 * kb, cudaMemcpyDeviceToDevice, c->stream));
-    }
+    uint32_t* mine = gat + (size_t)c->rank * 2 * c->k;
+    TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k)));
+    if (c->P > 1) TK_NCCL(c, ncclAllGather(mine, gat, 2 * c->k, ncclUint32, c->world, c->stream));
     mark(c, TK_STAGE_ALLGATHER);
     TK_TRY(decompress_impl(c, gat, c->P, c->k, c->d, out));
   } else {
-    // HiTopKComm (Alg. 2).  Step 1: intra-node reduce-scatter of g (Eq. 4) ...
+    // HiTopKComm (Alg. 2).  The compressed segment goes straight into this GPU's slot (its node
+    // index i = col_pos) of the column-gathered buffer.
+    uint32_t* gat = gathered ? gathered : c->recv;
+    uint32_t* mine = gat + (size_t)c->col_pos * 2 * c->k;
+    // Step 1: intra-node reduce-scatter of g (Eq. 4) ...
     if (c->cfg.rs_mode == TK_RS_ORDERED) {
       // ... ordered, read by this GPU's EF kernel straight from the row peers' buffers: make g
       // peer-visible, then a row barrier (stream-ordered all-reduce of 4 bytes) so every peer's
@@ -478,21 +478,16 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
       memset(&pr, 0, sizeof(pr));
       for (uint32_t q = 0; q < c->n; ++q) pr.p[q] = c->peer_g[q] + (size_t)c->row_pos * c->L;
       // Step 2 (fused with step 1): MSTopK on the segment with k~ (Eq. 5), EF on the segment residual.
-      TK_TRY(compress_impl(c, nullptr, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k), &pr,
+      TK_TRY(compress_impl(c, nullptr, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k), &pr,
                            (int)c->n));
     } else {
       TK_NCCL(c, ncclReduceScatter(g, c->seg, c->L, ncclFloat32, ncclSum, c->row, c->stream));
       mark(c, TK_STAGE_REDUCE_SCATTER);
       // Step 2: MSTopK on the segment with k~ (Eq. 5), error feedback on the segment residual.
-      TK_TRY(compress_impl(c, c->seg, ef ? r : nullptr, send, reinterpret_cast<float*>(send + c->k)));
+      TK_TRY(compress_impl(c, c->seg, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k)));
     }
-    // Step 3: inter-node all-gather among the m GPUs at the same position j (Eq. 6) ...
-    uint32_t* gat = gathered ? gathered : c->recv;
-    if (c->m > 1) {
-      TK_NCCL(c, ncclAllGather(send, gat, 2 * c->k, ncclUint32, c->col, c->stream));
-    } else {
-      TK_CUDA(c, cudaMemcpyAsync(gat, send, 2 * kb, cudaMemcpyDeviceToDevice, c->stream));
-    }
+    // Step 3: inter-node all-gather among the m GPUs at the same position j (Eq. 6), in place ...
+    if (c->m > 1) TK_NCCL(c, ncclAllGather(mine, gat, 2 * c->k, ncclUint32, c->col, c->stream));
     mark(c, TK_STAGE_ALLGATHER);
     float* my_seg = out + (size_t)c->row_pos * c->L;
     if (c->cfg.step4 == TK_STEP4_DENSE) {

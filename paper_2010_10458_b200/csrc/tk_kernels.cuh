@@ -322,13 +322,28 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   const uint64_t u0 = ((uint64_t)blockIdx.x * WARPS + warp) * units_per_warp;
   double stk[24];
   uint32_t mx = 0;
+  // NP == 0: the next unit's loads are issued before this unit is reduced (one unit in flight
+  // ahead per warp); the peer-sum variant (NP > 0) keeps NP*4 loads per unit and no prefetch
+  constexpr bool PREF = false;  // measured: prefetching does not help this phase (it runs at ~94% of the copy peak)
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 ng[4] = {z4, z4, z4, z4}, nr[4] = {z4, z4, z4, z4};
+  bool nfull = units_per_warp > 0 && (u0 + 1) * ROUND <= n;
+  if (PREF && nfull) ef_load<EF, NP>(g, pr, r, u0 * ROUND + 4 * lane, ng, nr);
   for (uint32_t i = 0; i < units_per_warp; ++i) {
     const uint64_t u = u0 + i;
     const uint64_t base = u * ROUND + 4 * lane;
     float4 acc[4];
-    if ((u + 1) * ROUND <= n) {
+    const bool full = PREF ? nfull : ((u + 1) * ROUND <= n);
+    if (full) {
       float4 rv[4];
-      ef_load<EF, NP>(g, pr, r, base, acc, rv);
+      if (PREF) {
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) { acc[ch] = ng[ch]; rv[ch] = nr[ch]; }
+        nfull = (i + 1 < units_per_warp) && (u + 2) * ROUND <= n;
+        if (nfull) ef_load<EF, NP>(g, pr, r, base + ROUND, ng, nr);
+      } else {
+        ef_load<EF, NP>(g, pr, r, base, acc, rv);
+      }
       if (EF) {
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
@@ -355,6 +370,10 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
           v[e] = x;
         }
         acc[ch] = make_float4(v[0], v[1], v[2], v[3]);
+      }
+      if (PREF) {
+        nfull = (i + 1 < units_per_warp) && (u + 2) * ROUND <= n;
+        if (nfull) ef_load<EF, NP>(g, pr, r, base + ROUND, ng, nr);
       }
     }
     double cs[4];
@@ -513,103 +532,86 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
       }
     }
   } else {
+    // Whole slab.  Lane l owns the 16 consecutive elements [16l, 16l + 16) of each 512-element
+    // round (four 128-bit loads; a warp instruction touches every other 16 B, its neighbour
+    // instruction the rest, through L1), so (lane, j) order is index order and the compaction
+    // needs one warp scan per round.
     uint32_t ncomp = 0;  // FIRST: entries appended by this warp so far
-    // FIRST: append the round's elements >= the compaction key in index order (chunk, lane,
-    // element); one packed warp scan covers the four chunks
-    auto compact = [&](uint4 v0, uint4 v1, uint4 v2, uint4 v3, uint64_t rbase, uint32_t valid) {
-      const uint4 v[4] = {v0, v1, v2, v3};
-      uint32_t m = 0;
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        m |= ((uint32_t)(kcmp1 - (int32_t)(v[ch].x & 0x7FFFFFFFu)) >> 31) << (4 * ch);
-        m |= ((uint32_t)(kcmp1 - (int32_t)(v[ch].y & 0x7FFFFFFFu)) >> 31) << (4 * ch + 1);
-        m |= ((uint32_t)(kcmp1 - (int32_t)(v[ch].z & 0x7FFFFFFFu)) >> 31) << (4 * ch + 2);
-        m |= ((uint32_t)(kcmp1 - (int32_t)(v[ch].w & 0x7FFFFFFFu)) >> 31) << (4 * ch + 3);
-      }
-      m &= valid;
+    auto append = [&](uint32_t m, uint64_t rbase) {
       if (!__any_sync(0xffffffffu, m != 0u)) return;
-      uint32_t packed = 0;  // per-chunk counts of this lane (<= 4) in bytes; warp sums <= 128
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) packed |= (uint32_t)__popc((m >> (4 * ch)) & 0xFu) << (8 * ch);
-      uint32_t incl = packed;
+      const uint32_t c = __popc(m);
+      uint32_t incl = c;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += o;
       }
       const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t excl = incl - packed;
+      uint32_t pos = ncomp + incl - c;
+      const uint32_t i0 = (uint32_t)(rbase + 16 * lane);
       uint32_t* oi = cp.idx + (size_t)gw * cp.C;
       uint32_t* ob = cp.bits + (size_t)gw * cp.C;
-      uint32_t chunk_base = ncomp;
-      const uint32_t i0 = (uint32_t)(rbase + 4 * lane);
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t pos = chunk_base + ((excl >> (8 * ch)) & 0xFFu);
-        const uint32_t mc = (m >> (4 * ch)) & 0xFu;
-        const uint32_t vv[4] = {v[ch].x, v[ch].y, v[ch].z, v[ch].w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if ((mc >> e) & 1u) {
-            if (pos < cp.C) {
-              oi[pos] = i0 + ch * 128 + e;
-              ob[pos] = vv[e];
-            }
-            ++pos;
-          }
+#pragma unroll 1
+      for (uint32_t mm = m; mm; mm &= mm - 1u) {  // sparse: ~rho-ish of the elements
+        const uint32_t j = __ffs(mm) - 1;
+        if (pos < cp.C) {
+          oi[pos] = i0 + j;
+          ob[pos] = __ldg(a32 + i0 + j);  // the line was just read: an L1 hit
         }
-        chunk_base += (tot >> (8 * ch)) & 0xFFu;
+        ++pos;
       }
-      ncomp = chunk_base;
+      ncomp += tot;
+    };
+    auto round16 = [&](uint4 q0, uint4 q1, uint4 q2, uint4 q3, uint64_t rbase) {
+      const uint32_t w[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
+                              q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+      uint32_t m = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int32_t a = (int32_t)(w[j] & 0x7FFFFFFFu);
+#pragma unroll
+        for (int s = 0; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
+        if (MODE == COUNT_FIRST) m |= ((uint32_t)(kcmp1 - a) >> 31) << j;
+      }
+      if (MODE == COUNT_FIRST) append(m, rbase);
     };
     // two rounds of 128-bit loads in flight per lane while a round is counted
-    const uint64_t e0 = lo + 4 * lane;
+    const uint4* p4 = reinterpret_cast<const uint4*>(a32 + lo) + 4 * lane;
     const uint64_t nfull = (hi - lo) / ROUND;  // full rounds of this slab
     uint4 a0 = make_uint4(0u, 0u, 0u, 0u), a1 = a0, a2 = a0, a3 = a0, b0 = a0, b1 = a0, b2 = a0, b3 = a0;
-#define TK_LOAD(q0, q1, q2, q3, r)                                              \
-  do {                                                                        \
-    const uint4* p_ = reinterpret_cast<const uint4*>(a32 + e0 + (r) * ROUND); \
-    q0 = p_[0];                                                               \
-    q1 = p_[32];                                                              \
-    q2 = p_[64];                                                              \
-    q3 = p_[96];                                                              \
-  } while (0)
-#define TK_COUNT(q0, q1, q2, q3, r)                                                 \
-  do {                                                                            \
-    count1(q0.x); count1(q0.y); count1(q0.z); count1(q0.w);                       \
-    count1(q1.x); count1(q1.y); count1(q1.z); count1(q1.w);                       \
-    count1(q2.x); count1(q2.y); count1(q2.z); count1(q2.w);                       \
-    count1(q3.x); count1(q3.y); count1(q3.z); count1(q3.w);                       \
-    if (MODE == COUNT_FIRST) compact(q0, q1, q2, q3, lo + (r) * ROUND, 0xFFFFu); \
+#define TK_LOAD(q0, q1, q2, q3, r)   \
+  do {                               \
+    const uint4* p_ = p4 + (r) * 128; \
+    q0 = p_[0];                      \
+    q1 = p_[1];                      \
+    q2 = p_[2];                      \
+    q3 = p_[3];                      \
   } while (0)
     if (nfull > 0) TK_LOAD(a0, a1, a2, a3, 0);
     if (nfull > 1) TK_LOAD(b0, b1, b2, b3, 1);
     for (uint64_t i = 0; i < nfull; i += 2) {
-      TK_COUNT(a0, a1, a2, a3, i);
+      round16(a0, a1, a2, a3, lo + i * ROUND);
       if (i + 2 < nfull) TK_LOAD(a0, a1, a2, a3, i + 2);
       if (i + 1 < nfull) {
-        TK_COUNT(b0, b1, b2, b3, i + 1);
+        round16(b0, b1, b2, b3, lo + (i + 1) * ROUND);
         if (i + 3 < nfull) TK_LOAD(b0, b1, b2, b3, i + 3);
       }
     }
 #undef TK_LOAD
-#undef TK_COUNT
     const uint64_t base = lo + nfull * ROUND;
     if (base < hi) {  // ragged tail round (end of the vector only)
-      uint32_t w[16], valid = 0;
+      uint32_t m = 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const uint64_t i = base + 4 * lane + (j >> 2) * 128 + (j & 3);
-        w[j] = 0u;
+        const uint64_t i = base + 16 * lane + j;
         if (i < hi) {
-          w[j] = a32[i];
-          count1(w[j]);
-          valid |= 1u << j;
+          const int32_t a = (int32_t)(a32[i] & 0x7FFFFFFFu);
+#pragma unroll
+          for (int s = 0; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
+          if (MODE == COUNT_FIRST) m |= ((uint32_t)(kcmp1 - a) >> 31) << j;
         }
       }
-      if (MODE == COUNT_FIRST)
-        compact(make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]),
-                make_uint4(w[8], w[9], w[10], w[11]), make_uint4(w[12], w[13], w[14], w[15]), base, valid);
+      if (MODE == COUNT_FIRST) append(m, base);
     }
     if (MODE == COUNT_FIRST && lane == 0) {
       cp.cnt[gw] = ncomp;
@@ -977,6 +979,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   grid_sync(f.bar);
   stamp();
   stats_root(f.cta_sum, f.cta_max, f.sp, &sc, f.step, f.lev0);
+  stamp();
   // ---- A3-A5: count passes.  The first resolves lev0 levels on the whole vector and compacts;
   // when the compacted entries are exact for the rest, each further pass resolves up to HIST_LEV
   // levels on them at once (histogram pass), else up to 2 levels per pass on the whole vector.
