@@ -231,3 +231,22 @@ def test_compress_full_size_c2(tk, step):
     assert np.array_equal(_u32(idx), ref.sel.idx)
     assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32))
     assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32))
+
+
+def test_compress_full_size_c3(tk):
+    """BASELINE config 3's gradient (d = 110M, rho = 1e-3) on one rank, two EF steps."""
+    d, rho, N = 110_000_000, 0.001, 10
+    k = oracle.k_from_density(d, rho)
+    ctx = tk.Context(d, rho=rho, n_iters=N, seed=77)
+    r = np.zeros(d, np.float32)
+    rd = _dev(r)
+    for step in range(2):
+        g = gradgen.gradient(d, "G", cfg=3, step=step)
+        idx, val = ctx.compress(_dev(g), rd)
+        ref = oracle.compress(g, r, k, N, seed=77, step=step)
+        _check_stats(ctx.stats(), ref)
+        assert np.array_equal(_u32(idx), ref.sel.idx)
+        assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32))
+        assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32))
+        r = ref.residual
+        ctx.set_step(step + 1)
