@@ -100,6 +100,7 @@ typedef struct tk_stats {
   uint32_t nonfinite;      /* 1 if a NaN/Inf was seen (sticky)                                 */
   uint32_t compacted;      /* 1 if passes 2.. and the selection ran on the entries compacted by
                               the first count pass (an exact shortcut)          */
+  uint32_t n_compacted;    /* entries the first count pass kept (when compacted)                */
   uint32_t n_phases;       /* phase boundaries recorded in phase_ns                             */
   uint64_t phase_ns[8];    /* device %globaltimer (ns) at k_compress's phase boundaries (CTA 0,
                               after each grid barrier): start, stats, each count pass, prefix,

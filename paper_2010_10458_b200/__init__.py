@@ -50,7 +50,8 @@ class _Stats(ctypes.Structure):
                 ("key1", ctypes.c_uint32), ("key2", ctypes.c_uint32),
                 ("thres1_set", ctypes.c_uint32), ("thres2_set", ctypes.c_uint32),
                 ("len2", ctypes.c_uint64), ("rand_start", ctypes.c_uint64), ("step", ctypes.c_uint64),
-                ("nonfinite", ctypes.c_uint32), ("compacted", ctypes.c_uint32), ("n_phases", ctypes.c_uint32),
+                ("nonfinite", ctypes.c_uint32), ("compacted", ctypes.c_uint32), ("n_compacted", ctypes.c_uint32),
+                ("n_phases", ctypes.c_uint32),
                 ("phase_ns", ctypes.c_uint64 * 8)]
 
 
@@ -169,6 +170,7 @@ class Stats:
     step: int
     nonfinite: bool
     compacted: bool
+    n_compacted: int
     phase_us: list  # k_compress phase durations (device globaltimer, CTA 0)
 
 
@@ -281,7 +283,7 @@ class Context:
         return Stats(mean=s.mean, max_bits=s.max_bits, trials=trials, k=s.k, k1=s.k1, k2=s.k2, thres1=s.thres1,
                      thres2=s.thres2, thres1_set=bool(s.thres1_set), thres2_set=bool(s.thres2_set), key1=s.key1,
                      key2=s.key2, len2=s.len2, rand=s.rand_start, step=s.step, nonfinite=bool(s.nonfinite),
-                     compacted=bool(s.compacted),
+                     compacted=bool(s.compacted), n_compacted=int(s.n_compacted),
                      phase_us=[(s.phase_ns[i + 1] - s.phase_ns[i]) / 1e3 for i in range(max(0, s.n_phases - 1))])
 
     def input_buffer(self):

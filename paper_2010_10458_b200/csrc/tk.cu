@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -223,13 +224,13 @@ tk_status plan_launches(tk_ctx* c) {
   // persistent cooperative grid: every CTA resident; no more CTAs than warp rounds of work
   c->grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sms * occ, (rounds + WARPS - 1) / WARPS));
   c->W = c->grid * WARPS;
-  c->S = ((L + c->W - 1) / c->W + ROUND - 1) / ROUND * ROUND;  // whole rounds: no ragged slab ends
   uint64_t upw = 1;  // ef phase: aligned power-of-two run of units per warp covering the vector
   while ((uint64_t)c->W * upw < rounds) upw <<= 1;
   c->units_per_warp = (uint32_t)upw;
+  c->S = upw * ROUND;  // count / select slabs = the ef phase's warp runs (acc is re-read from L2)
   TK_TRY(dev_alloc(c, &c->cta_sum, c->grid));
   TK_TRY(dev_alloc(c, &c->cta_max, c->grid));
-  TK_TRY(dev_alloc(c, &c->cta_cls, 2 * (size_t)c->grid));
+  TK_TRY(dev_alloc(c, &c->cta_cls, 3 * (size_t)c->grid));
   TK_TRY(dev_alloc(c, &c->totals, (size_t)HIST_BINS * c->npass));
   TK_TRY(dev_alloc(c, &c->bar, 4));
   TK_CUDA(c, cudaMemset(c->bar, 0, 4 * sizeof(uint32_t)));
@@ -355,10 +356,13 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   // whole vector; later passes take up to `levels` levels on the compacted entries, or up to 2 on
   // the whole vector.  Scratch is sized for the worst case (all passes on the whole vector).
   {
-    const uint32_t first = std::min<uint32_t>(std::min<uint32_t>(2u, c->levels), k.n_iters);
+    // first pass: up to 3 keys along the predicted path (at least one level resolved)
+    uint32_t keys = 3;  // tuning knob (TK_FIRST_KEYS=1..3); results do not depend on it
+    if (const char* e = getenv("TK_FIRST_KEYS")) keys = std::max(1, std::min(3, atoi(e)));
+    const uint32_t first = std::min<uint32_t>(std::min<uint32_t>(keys, c->levels), k.n_iters);
     c->lev_sched[0] = (int)first;
     const uint32_t per = std::min<uint32_t>(2u, c->levels);
-    c->npass = 1 + (k.n_iters - first + per - 1) / per;
+    c->npass = 1 + (k.n_iters - 1 + per - 1) / per;  // worst case: the first pass resolves one level
   }
   auto bail = [&](tk_status s) {
     free_all(c);
@@ -568,6 +572,7 @@ tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
   c->nonfinite_sticky |= h.nonfinite;
   st->nonfinite = c->nonfinite_sticky;
   st->compacted = h.cap_ok;
+  st->n_compacted = h.n_compacted;
   st->n_phases = std::min<uint32_t>(8, h.n_phase);
   for (int i = 0; i < 8; ++i) st->phase_ns[i] = h.phase_ns[i];
   if (c->nonfinite_sticky) return fail(c, TK_ERR_NONFINITE, "non-finite value in acc (precondition, Q24)");

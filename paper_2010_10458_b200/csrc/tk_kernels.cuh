@@ -56,6 +56,7 @@ struct Ctrl {
   uint64_t phase_ns[8];  // %globaltimer at the phase boundaries of the last k_compress (CTA 0)
   uint32_t n_phase;
   uint32_t n_compacted;  // entries kept by the first count pass (all warps)
+  uint32_t cand_tree;    // the candidates form a complete subtree (walked by index in replay)
 };
 
 // Per-launch parameters of the MSTopK kernels.  The count and selection kernels share one
@@ -71,8 +72,8 @@ struct SearchParams {
 };
 
 // Compacted entries of the first count pass: warp w keeps, in ascending index order, every
-// element of its slab with |acc| >= the pass's lowest candidate key (idx[w*C + j], bits[w*C + j],
-// j < cnt[w]).  When the bisection's bracket after that pass lies above that key, no later trial
+// element of its slab with |acc| >= the compaction key, at the top of its region
+// (idx[w*C + C - cnt[w] + j], bits[...], j < cnt[w]).  When the bisection's bracket after that pass lies above that key, no later trial
 // threshold and no selected element can lie below it, so the later passes and the selection read
 // only these entries instead of the whole vector (exact: same counts, same sets).
 struct Compact {
@@ -99,6 +100,11 @@ __device__ __forceinline__ double threshold_of(double abar, double U, double rat
   return __dadd_rn(abar, __dmul_rn(ratio, __dsub_rn(U, abar)));
 }
 // smallest fp32 >= t, as bits: a >= t  <=>  bits(a) >= key for finite a >= 0 (Q4)
+// four consecutive u32 of the compacted entries (their start is only 4-byte aligned)
+__device__ __forceinline__ uint4 ldcg4(const uint32_t* p) {
+  return make_uint4(__ldcg(p), __ldcg(p + 1), __ldcg(p + 2), __ldcg(p + 3));
+}
+
 __device__ __forceinline__ uint32_t key_of(double t) {
   if (!(t > 0.0)) return 0u;
   return __float_as_uint(__double2float_ru(t));
@@ -120,17 +126,34 @@ __device__ void make_candidates_par(Ctrl* c, int lev) {
     c->cand_t[m - 1] = t;
     c->cand_key[m - 1] = key_of(t);
   }
-  if (threadIdx.x == 0) c->ncand = (uint32_t)T;
+  if (threadIdx.x == 0) {
+    c->ncand = (uint32_t)T;
+    c->cand_tree = 1u;
+  }
 }
 
 // Replay lev levels of Alg. 1 l.8-23 on the candidates' exact counts.
-__device__ void replay_levels(Ctrl* c, const uint32_t* totals, int lev, int pass, uint64_t k) {
-  int m = 1 << (lev - 1);
-  int stepm = m >> 1;
-  for (int l = 0; l < lev; ++l) {
-    const int s = m - 1;
+__device__ int replay_levels(Ctrl* c, const uint32_t* totals, int max_lev, int pass, uint64_t k) {
+  // Alg. 1 l.8-23, one level at a time: the level's ratio l + (r-l)/2 (exact, Q5) is looked up
+  // among the counted candidates; the replay stops at the first level whose threshold was not
+  // counted (speculative candidate sets).  Returns the number of levels resolved.
+  const int nc = (int)c->ncand;
+  // a complete subtree (make_candidates_par: 2^L - 1 ascending candidates) is walked by index;
+  // other sets (the first pass's path) are searched
+  const bool tree = ((nc + 1) & nc) == 0 && c->cand_tree;
+  int m = (nc + 1) >> 1, stepm = m >> 1;  // tree walk: 1-based node index and half-width
+  int l = 0;
+  for (; l < max_lev; ++l) {
+    const double ratio = __dadd_rn(c->lo, __dmul_rn(__dsub_rn(c->hi, c->lo), 0.5));  // Alg. 1 l.8
+    int s = -1;
+    if (tree) {
+      if (m >= 1 && m <= nc && c->cand_ratio[m - 1] == ratio) s = m - 1;
+    } else {
+      for (int q = 0; q < nc; ++q)
+        if (c->cand_ratio[q] == ratio) { s = q; break; }
+    }
+    if (s < 0) break;
     const uint32_t nnz = totals[s];
-    const double ratio = c->cand_ratio[s];
     const double t = c->cand_t[s];
     const uint32_t key = c->cand_key[s];
     const uint32_t it = c->it;
@@ -154,6 +177,24 @@ __device__ void replay_levels(Ctrl* c, const uint32_t* totals, int lev, int pass
     }
     stepm >>= 1;
   }
+  return l;
+}
+
+// Speculative candidates of the first pass: the lev bisection nodes along the path toward
+// `target` (the bracket the previous compression ended in).  When the data take that path, one
+// read of the vector resolves lev levels with lev keys; otherwise it resolves at least one.
+__device__ void make_candidates_path(Ctrl* c, int lev, double target) {
+  double lo = c->lo, hi = c->hi;
+  for (int q = 0; q < lev; ++q) {
+    const double ratio = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), 0.5));
+    const double t = threshold_of(c->abar, c->U, ratio);
+    c->cand_ratio[q] = ratio;
+    c->cand_t[q] = t;
+    c->cand_key[q] = key_of(t);
+    if (target >= ratio) lo = ratio; else hi = ratio;
+  }
+  c->ncand = (uint32_t)lev;
+  c->cand_tree = 0u;
 }
 
 // Alg. 1 l.27 window: R = len(iota2) - (k - k1) + 1 >= 1 (Q8, Q9); rand uniform on [0, R).
@@ -459,14 +500,17 @@ __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* _
     stats_finalize(sc, sp, s_v[0], m, step, first_levels);
   }
   __syncthreads();
-  make_candidates_par(sc, first_levels);
-  __syncthreads();
   if (tid == 0) {
+    make_candidates_path(sc, first_levels, sc->prev_lo);
     // compaction key of the first count pass: the highest of its candidates at or below the
     // bracket the previous compression ended in (any choice is exact; a good one keeps few elements)
     int ms = 0;
     for (int q = 1; q < (int)sc->ncand; ++q)
-      if (sc->cand_ratio[q] <= sc->prev_lo) ms = q;
+      if (sc->cand_ratio[q] <= sc->prev_lo && sc->cand_ratio[q] > sc->cand_ratio[ms]) ms = q;
+    if (sc->cand_ratio[ms] > sc->prev_lo) {  // no candidate below the prediction: take the lowest
+      for (int q = 1; q < (int)sc->ncand; ++q)
+        if (sc->cand_ratio[q] < sc->cand_ratio[ms]) ms = q;
+    }
     sc->cmp_key = sc->cand_key[ms];
     sc->cmp_ratio = sc->cand_ratio[ms];
   }
@@ -486,11 +530,11 @@ __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* _
 // HBM/L2: 4 B/elem (FIRST, FULL), 4 B/entry (CAP); FIRST also writes 8 B per compacted entry.
 enum { COUNT_FIRST = 0, COUNT_CAP = 1, COUNT_FULL = 2 };
 
-template <int LEV, int MODE>
+template <int NK, int MODE>
 __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const Ctrl* sc, const SearchParams sp,
                                             uint32_t* __restrict__ wcnt, const Compact cp, uint32_t* totals,
                                             uint32_t* overflow, int pass) {
-  constexpr int T = (1 << LEV) - 1;
+  constexpr int T = NK;  // keys counted in this pass
   __shared__ uint32_t s_cnt[WARPS][16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int32_t km1[T];  // key - 1: a >= key  <=>  (key - 1 - a) < 0 (no overflow for 0 <= a, key < 2^31)
@@ -511,7 +555,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
   };
   if (MODE == COUNT_CAP) {
     const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-    const uint32_t* eb = cp.bits + (size_t)gw * cp.C;
+    const uint32_t* eb = cp.bits + (size_t)gw * cp.C + (cp.C - ne);  // entries sit at the region's top
     // this warp's entry loads in flight together (4 x 128 entries per iteration)
     for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
       uint4 q[4];
@@ -519,7 +563,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
       for (int u = 0; u < 4; ++u) {
         const uint32_t j = j0 + u * 128 + 4 * lane;
         q[u] = make_uint4(0u, 0u, 0u, 0u);
-        if (j + 4 <= ne) q[u] = __ldcg(reinterpret_cast<const uint4*>(eb + j));
+        if (j + 4 <= ne) q[u] = ldcg4(eb + j);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -536,7 +580,11 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
     // round (four 128-bit loads; a warp instruction touches every other 16 B, its neighbour
     // instruction the rest, through L1), so (lane, j) order is index order and the compaction
     // needs one warp scan per round.
-    uint32_t ncomp = 0;  // FIRST: entries appended by this warp so far
+    // The slab is walked from its END to its start: the slabs coincide with the ef phase's warp
+    // runs, so the most recently written (still L2-resident) part of acc is read first.  The
+    // compacted entries are therefore filled from the top of the warp's region downward and end
+    // up in ascending index order in [C - count, C).
+    uint32_t ncomp = 0;  // FIRST: entries kept by this warp so far
     auto append = [&](uint32_t m, uint64_t rbase) {
       if (!__any_sync(0xffffffffu, m != 0u)) return;
       const uint32_t c = __popc(m);
@@ -547,14 +595,14 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
         if (lane >= off) incl += o;
       }
       const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-      uint32_t pos = ncomp + incl - c;
+      int64_t pos = (int64_t)cp.C - (int64_t)ncomp - (int64_t)tot + (int64_t)(incl - c);
       const uint32_t i0 = (uint32_t)(rbase + 16 * lane);
       uint32_t* oi = cp.idx + (size_t)gw * cp.C;
       uint32_t* ob = cp.bits + (size_t)gw * cp.C;
 #pragma unroll 1
-      for (uint32_t mm = m; mm; mm &= mm - 1u) {  // sparse: ~rho-ish of the elements
+      for (uint32_t mm = m; mm; mm &= mm - 1u) {  // sparse: a few percent of the elements at most
         const uint32_t j = __ffs(mm) - 1;
-        if (pos < cp.C) {
+        if (pos >= 0) {
           oi[pos] = i0 + j;
           ob[pos] = __ldg(a32 + i0 + j);  // the line was just read: an L1 hit
         }
@@ -575,9 +623,24 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
       }
       if (MODE == COUNT_FIRST) append(m, rbase);
     };
-    // two rounds of 128-bit loads in flight per lane while a round is counted
     const uint4* p4 = reinterpret_cast<const uint4*>(a32 + lo) + 4 * lane;
     const uint64_t nfull = (hi - lo) / ROUND;  // full rounds of this slab
+    const uint64_t tbase = lo + nfull * ROUND;
+    if (tbase < hi) {  // ragged tail round (end of the vector only): first, in reverse order
+      uint32_t m = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint64_t i = tbase + 16 * lane + j;
+        if (i < hi) {
+          const int32_t a = (int32_t)(a32[i] & 0x7FFFFFFFu);
+#pragma unroll
+          for (int s = 0; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
+          if (MODE == COUNT_FIRST) m |= ((uint32_t)(kcmp1 - a) >> 31) << j;
+        }
+      }
+      if (MODE == COUNT_FIRST) append(m, tbase);
+    }
+    // two rounds of 128-bit loads in flight per lane while a round is counted (last round first)
     uint4 a0 = make_uint4(0u, 0u, 0u, 0u), a1 = a0, a2 = a0, a3 = a0, b0 = a0, b1 = a0, b2 = a0, b3 = a0;
 #define TK_LOAD(q0, q1, q2, q3, r)   \
   do {                               \
@@ -587,32 +650,17 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
     q2 = p_[2];                      \
     q3 = p_[3];                      \
   } while (0)
-    if (nfull > 0) TK_LOAD(a0, a1, a2, a3, 0);
-    if (nfull > 1) TK_LOAD(b0, b1, b2, b3, 1);
+    if (nfull > 0) TK_LOAD(a0, a1, a2, a3, nfull - 1);
+    if (nfull > 1) TK_LOAD(b0, b1, b2, b3, nfull - 2);
     for (uint64_t i = 0; i < nfull; i += 2) {
-      round16(a0, a1, a2, a3, lo + i * ROUND);
-      if (i + 2 < nfull) TK_LOAD(a0, a1, a2, a3, i + 2);
+      round16(a0, a1, a2, a3, lo + (nfull - 1 - i) * ROUND);
+      if (i + 2 < nfull) TK_LOAD(a0, a1, a2, a3, nfull - 3 - i);
       if (i + 1 < nfull) {
-        round16(b0, b1, b2, b3, lo + (i + 1) * ROUND);
-        if (i + 3 < nfull) TK_LOAD(b0, b1, b2, b3, i + 3);
+        round16(b0, b1, b2, b3, lo + (nfull - 2 - i) * ROUND);
+        if (i + 3 < nfull) TK_LOAD(b0, b1, b2, b3, nfull - 4 - i);
       }
     }
 #undef TK_LOAD
-    const uint64_t base = lo + nfull * ROUND;
-    if (base < hi) {  // ragged tail round (end of the vector only)
-      uint32_t m = 0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint64_t i = base + 16 * lane + j;
-        if (i < hi) {
-          const int32_t a = (int32_t)(a32[i] & 0x7FFFFFFFu);
-#pragma unroll
-          for (int s = 0; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
-          if (MODE == COUNT_FIRST) m |= ((uint32_t)(kcmp1 - a) >> 31) << j;
-        }
-      }
-      if (MODE == COUNT_FIRST) append(m, base);
-    }
     if (MODE == COUNT_FIRST && lane == 0) {
       cp.cnt[gw] = ncomp;
       if (ncomp > cp.C) atomicOr(overflow, 1u);
@@ -661,7 +709,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
   __syncthreads();
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-  const uint32_t* eb = cp.bits + (size_t)gw * cp.C;
+  const uint32_t* eb = cp.bits + (size_t)gw * cp.C + (cp.C - ne);  // entries sit at the region's top
   auto add = [&](uint32_t bits) {
     const int32_t a = (int32_t)(bits & 0x7FFFFFFFu);
     uint32_t b = 0;
@@ -675,7 +723,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
     for (int u = 0; u < 4; ++u) {
       const uint32_t j = j0 + u * 128 + 4 * lane;
       q[u] = make_uint4(0u, 0u, 0u, 0u);
-      if (j + 4 <= ne) q[u] = __ldcg(reinterpret_cast<const uint4*>(eb + j));
+      if (j + 4 <= ne) q[u] = ldcg4(eb + j);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -737,14 +785,14 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
     // ---- compacted entries of this warp (ascending index order): 128 per iteration, lane l
     // holds entries 4l..4l+3 of the group, so (lane, e) order is index order ----
     const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-    const uint32_t* ei = cp.idx + (size_t)gw * cp.C;
-    const uint32_t* eb = cp.bits + (size_t)gw * cp.C;
+    const uint32_t* ei = cp.idx + (size_t)gw * cp.C + (cp.C - ne);  // entries sit at the region's top
+    const uint32_t* eb = cp.bits + (size_t)gw * cp.C + (cp.C - ne);
     for (uint32_t j0 = 0; j0 < ne; j0 += 128) {
       const uint32_t j = j0 + 4 * lane;
       uint32_t bb[4] = {0u, 0u, 0u, 0u}, ii[4] = {0u, 0u, 0u, 0u};
       if (j + 4 <= ne) {
-        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(eb + j));
-        const uint4 x = __ldcg(reinterpret_cast<const uint4*>(ei + j));
+        const uint4 q = ldcg4(eb + j);
+        const uint4 x = ldcg4(ei + j);
         bb[0] = q.x; bb[1] = q.y; bb[2] = q.z; bb[3] = q.w;
         ii[0] = x.x; ii[1] = x.y; ii[2] = x.z; ii[3] = x.w;
       } else {
@@ -949,9 +997,9 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-template <int LEV, int MODE>
+template <int NK, int MODE>
 __device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass) {
-  count_phase<LEV, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * pass, f.flags, pass);
+  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * pass, f.flags, pass);
 }
 
 template <bool EF, int NP>
@@ -961,6 +1009,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   __shared__ HistSmem s_hist;
   __shared__ uint32_t s_w[2][WARPS];
   __shared__ uint32_t s_base[2];
+  __shared__ uint32_t s_ne[WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)
   int nph = 0;
@@ -972,7 +1021,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   stamp();
   if (blockIdx.x == 0) {
     for (int i = tid; i < HIST_BINS * f.max_pass; i += THREADS) f.totals[i] = 0u;
-    if (tid == 0) f.flags[0] = 0u;
+    if (tid == 0) { f.flags[0] = 0u; f.flags[1] = 0u; }
   }
   // ---- A1-A2: error feedback, |acc| pairwise tree and max ----
   ef_phase<EF, NP>(f.g, f.pr, f.r, f.sp, f.units_per_warp, f.cta_sum, f.cta_max);
@@ -985,14 +1034,17 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   // levels on them at once (histogram pass), else up to 2 levels per pass on the whole vector.
   // The bits do not depend on this schedule. ----
   const int N = (int)f.n_iters;
+  __shared__ int s_got;
   int done = 0;
   for (int p = 0; done < N; ++p) {
     int lev;
     bool hist = false;
     uint32_t* tot_p = f.totals + HIST_BINS * p;
     if (p == 0) {
-      lev = f.lev0;
-      if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, 0); else run_count<2, COUNT_FIRST>(f, &sc, 0);
+      lev = f.lev0;  // keys along the predicted path
+      if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, 0);
+      else if (lev == 2) run_count<2, COUNT_FIRST>(f, &sc, 0);
+      else run_count<3, COUNT_FIRST>(f, &sc, 0);
     } else if (sc.cap_ok) {
       hist = true;
       lev = min(min(HIST_LEV, f.cap_levels), N - done);
@@ -1008,9 +1060,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       }
     } else {
       lev = min(min(2, f.cap_levels), N - done);
-      if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<2, COUNT_FULL>(f, &sc, p);
+      if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<3, COUNT_FULL>(f, &sc, p);
     }
-    done += lev;
     grid_sync(f.bar);
     stamp();
     if (hist) {
@@ -1021,34 +1072,39 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     }
     if (tid == 0) {
       const double cmp_ratio = sc.cmp_ratio;
-      replay_levels(&sc, s_tot, lev, p, f.sp.k);
+      s_got = replay_levels(&sc, s_tot, min(lev, N - done), p, f.sp.k);
       if (p == 0) {
         // compacted mode is exact iff every later threshold (and thres2) lies above the compaction
         // key: the bracket's lower end must have reached its ratio, and nothing overflowed
         sc.cap_ok = (sc.lo >= cmp_ratio && __ldcg(f.flags) == 0u) ? 1u : 0u;
       }
-      if (done == N) finish_window(&sc, f.sp);
+      if (done + s_got == N) finish_window(&sc, f.sp);
     }
     __syncthreads();
+    done += s_got;
     if (done < N) {
       const int next = sc.cap_ok ? min(min(HIST_LEV, f.cap_levels), N - done) : min(min(2, f.cap_levels), N - done);
       make_candidates_par(&sc, next);
       __syncthreads();
     }
   }
+  stamp();
   // ---- A7 prefix: class-1 / class-2 counts of each warp slab, then of the CTAs before it ----
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint32_t W = f.sp.W;
   const uint64_t slo = min(f.sp.n, (uint64_t)gw * f.sp.S);
   const uint64_t shi = min(f.sp.n, slo + f.sp.S);
   uint32_t c1 = 0, call = 0;
+  if (lane == 0) s_ne[warp] = 0u;
   if (sc.cap_ok) {
     // count the warp's compacted entries at key1 / key2 directly (exact: both keys lie at or
     // above every element excluded from the entries)
     const int32_t k1m1 = sc.prov1 >= 0 ? (int32_t)sc.key1 - 1 : 0x7FFFFFFF;
     const int32_t k2m1 = (int32_t)sc.key2 - 1;
     const uint32_t ne = min(__ldcg(f.cp.cnt + gw), f.cp.C);
-    const uint32_t* eb = f.cp.bits + (size_t)gw * f.cp.C;
+    const uint32_t* eb = f.cp.bits + (size_t)gw * f.cp.C + (f.cp.C - ne);
+    if (lane == 0) s_ne[warp] = ne;
+#pragma unroll 4
     for (uint32_t j = lane; j < ne; j += 32) {
       const int32_t a = (int32_t)(__ldcg(eb + j) & 0x7FFFFFFFu);
       c1 += (uint32_t)(k1m1 - a) >> 31;
@@ -1067,10 +1123,11 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   }
   __syncthreads();
   if (tid == 0) {
-    uint32_t t1 = 0, t2 = 0;
-    for (int w = 0; w < WARPS; ++w) { t1 += s_w[0][w]; t2 += s_w[1][w]; }
+    uint32_t t1 = 0, t2 = 0, tn = 0;
+    for (int w = 0; w < WARPS; ++w) { t1 += s_w[0][w]; t2 += s_w[1][w]; tn += s_ne[w]; }
     f.cta_cls[blockIdx.x] = t1;
     f.cta_cls[gridDim.x + blockIdx.x] = t2;
+    f.cta_cls[2 * gridDim.x + blockIdx.x] = tn;  // compacted entries (statistics)
   }
   grid_sync(f.bar);
   stamp();
@@ -1098,7 +1155,19 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   // ---- A7-A8: selection, compaction, residual write-back ----
   select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, f.idx_out, f.val_out, EF ? f.r : nullptr, f.cp);
   stamp();
-  if (blockIdx.x == 0) ctrl_to_global(f.c, &sc);
+  if (blockIdx.x == 0) {
+    uint32_t tn = 0;
+    for (uint32_t b = tid; b < gridDim.x; b += THREADS) tn += __ldcg(f.cta_cls + 2 * gridDim.x + b);
+    tn = __reduce_add_sync(0xffffffffu, tn);
+    if (lane == 0) s_w[0][warp] = tn;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < WARPS; ++w) t += s_w[0][w];
+      sc.n_compacted = sc.cap_ok ? t : 0u;
+    }
+    ctrl_to_global(f.c, &sc);
+  }
 }
 
 // ------------------------------------------------------------------------------------------

@@ -20,6 +20,7 @@ for s in range(steps):
         st = ctx.stats()
         acc = st.phase_us if acc is None else [a + b for a, b in zip(acc, st.phase_us)]
 n = steps - 20
-names = ["ef", "root"] + [f"pass{i}" for i in range(len(acc) - 4)] + ["prefix", "select"]
+names = ["ef", "root"] + [f"pass{i}" for i in range(len(acc) - 5)] + ["replay", "prefix", "select"]
 print("phases (us):", {names[i] if i < len(names) else i: round(v / n, 1) for i, v in enumerate(acc)},
-      "total", round(sum(acc) / n, 1), "compacted", st.compacted)
+      "total", round(sum(acc) / n, 1), "compacted", st.compacted, "n_compacted", st.n_compacted,
+      "frac", round(st.n_compacted / d, 4))
