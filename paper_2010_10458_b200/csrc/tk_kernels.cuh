@@ -511,8 +511,16 @@ __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* _
       for (int q = 1; q < (int)sc->ncand; ++q)
         if (sc->cand_ratio[q] < sc->cand_ratio[ms]) ms = q;
     }
-    sc->cmp_key = sc->cand_key[ms];
-    sc->cmp_ratio = sc->cand_ratio[ms];
+    // the compaction key becomes candidate 0, so the first pass's compaction test is the same
+    // compare as its count of that key (the replay finds candidates by ratio, order-free)
+    if (ms != 0) {
+      const double r0 = sc->cand_ratio[0], t0 = sc->cand_t[0];
+      const uint32_t k0 = sc->cand_key[0];
+      sc->cand_ratio[0] = sc->cand_ratio[ms]; sc->cand_t[0] = sc->cand_t[ms]; sc->cand_key[0] = sc->cand_key[ms];
+      sc->cand_ratio[ms] = r0; sc->cand_t[ms] = t0; sc->cand_key[ms] = k0;
+    }
+    sc->cmp_key = sc->cand_key[0];
+    sc->cmp_ratio = sc->cand_ratio[0];
   }
   __syncthreads();
 }
@@ -585,43 +593,54 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
     // compacted entries are therefore filled from the top of the warp's region downward and end
     // up in ascending index order in [C - count, C).
     uint32_t ncomp = 0;  // FIRST: entries kept by this warp so far
-    auto append = [&](uint32_t m, uint64_t rbase) {
-      if (!__any_sync(0xffffffffu, m != 0u)) return;
-      const uint32_t c = __popc(m);
-      uint32_t incl = c;
+    // two rounds' entries with one warp scan (16-bit packed per-lane counts); round A holds the
+    // higher indices so its block goes above round B's (entries descend from the region's top)
+    auto append2 = [&](uint32_t ma, uint64_t ra, uint32_t mb, uint64_t rb) {
+      if (!__any_sync(0xffffffffu, (ma | mb) != 0u)) return;
+      const uint32_t ca = __popc(ma), cb = __popc(mb);
+      const uint32_t packed = ca | (cb << 16);
+      uint32_t incl = packed;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += o;
       }
       const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-      int64_t pos = (int64_t)cp.C - (int64_t)ncomp - (int64_t)tot + (int64_t)(incl - c);
-      const uint32_t i0 = (uint32_t)(rbase + 16 * lane);
+      const uint32_t excl = incl - packed;
+      const uint32_t ta = tot & 0xFFFFu, tb = tot >> 16;
       uint32_t* oi = cp.idx + (size_t)gw * cp.C;
       uint32_t* ob = cp.bits + (size_t)gw * cp.C;
+      int64_t pa = (int64_t)cp.C - (int64_t)ncomp - (int64_t)ta + (int64_t)(excl & 0xFFFFu);
+      int64_t pb = (int64_t)cp.C - (int64_t)ncomp - (int64_t)ta - (int64_t)tb + (int64_t)(excl >> 16);
+      const uint32_t ia = (uint32_t)(ra + 16 * lane), ib = (uint32_t)(rb + 16 * lane);
 #pragma unroll 1
-      for (uint32_t mm = m; mm; mm &= mm - 1u) {  // sparse: a few percent of the elements at most
+      for (uint32_t mm = ma; mm; mm &= mm - 1u) {
         const uint32_t j = __ffs(mm) - 1;
-        if (pos >= 0) {
-          oi[pos] = i0 + j;
-          ob[pos] = __ldg(a32 + i0 + j);  // the line was just read: an L1 hit
-        }
-        ++pos;
+        if (pa >= 0) { oi[pa] = ia + j; ob[pa] = __ldg(a32 + ia + j); }
+        ++pa;
       }
-      ncomp += tot;
+#pragma unroll 1
+      for (uint32_t mm = mb; mm; mm &= mm - 1u) {
+        const uint32_t j = __ffs(mm) - 1;
+        if (pb >= 0) { oi[pb] = ib + j; ob[pb] = __ldg(a32 + ib + j); }
+        ++pb;
+      }
+      ncomp += ta + tb;
     };
-    auto round16 = [&](uint4 q0, uint4 q1, uint4 q2, uint4 q3, uint64_t rbase) {
+    auto round16 = [&](uint4 q0, uint4 q1, uint4 q2, uint4 q3) -> uint32_t {
       const uint32_t w[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
                               q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
       uint32_t m = 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int32_t a = (int32_t)(w[j] & 0x7FFFFFFFu);
+        const bool p0 = a > km1[0];  // key 0 (= the compaction key in the first pass)
+        cnt[0] += p0 ? 1u : 0u;
+        if (MODE == COUNT_FIRST && p0) m |= 1u << j;
 #pragma unroll
-        for (int s = 0; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
-        if (MODE == COUNT_FIRST) m |= ((uint32_t)(kcmp1 - a) >> 31) << j;
+        for (int s = 1; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
       }
-      if (MODE == COUNT_FIRST) append(m, rbase);
+      return m;
     };
     const uint4* p4 = reinterpret_cast<const uint4*>(a32 + lo) + 4 * lane;
     const uint64_t nfull = (hi - lo) / ROUND;  // full rounds of this slab
@@ -638,7 +657,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
           if (MODE == COUNT_FIRST) m |= ((uint32_t)(kcmp1 - a) >> 31) << j;
         }
       }
-      if (MODE == COUNT_FIRST) append(m, tbase);
+      if (MODE == COUNT_FIRST) append2(m, tbase, 0u, 0u);
     }
     // two rounds of 128-bit loads in flight per lane while a round is counted (last round first)
     uint4 a0 = make_uint4(0u, 0u, 0u, 0u), a1 = a0, a2 = a0, a3 = a0, b0 = a0, b1 = a0, b2 = a0, b3 = a0;
@@ -653,12 +672,15 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
     if (nfull > 0) TK_LOAD(a0, a1, a2, a3, nfull - 1);
     if (nfull > 1) TK_LOAD(b0, b1, b2, b3, nfull - 2);
     for (uint64_t i = 0; i < nfull; i += 2) {
-      round16(a0, a1, a2, a3, lo + (nfull - 1 - i) * ROUND);
+      const uint32_t ma = round16(a0, a1, a2, a3);
       if (i + 2 < nfull) TK_LOAD(a0, a1, a2, a3, nfull - 3 - i);
+      uint32_t mb = 0;
       if (i + 1 < nfull) {
-        round16(b0, b1, b2, b3, lo + (nfull - 2 - i) * ROUND);
+        mb = round16(b0, b1, b2, b3);
         if (i + 3 < nfull) TK_LOAD(b0, b1, b2, b3, nfull - 4 - i);
       }
+      // one append for the pair: round A (higher indices) above round B in the region
+      if (MODE == COUNT_FIRST) append2(ma, lo + (nfull - 1 - i) * ROUND, mb, lo + (nfull - 2 - i) * ROUND);
     }
 #undef TK_LOAD
     if (MODE == COUNT_FIRST && lane == 0) {
