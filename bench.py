@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--group-size", type=int, default=1, help="HiTopKComm n (1 = flat NaiveAG)")
     ap.add_argument("--step4", default="dense", choices=["dense", "sparse"])
     ap.add_argument("--levels", type=int, default=0, help="bisection levels per count pass (0 = default)")
+    ap.add_argument("--ag-mode", default="push", choices=["push", "nccl"], help="flat all-gather: fused peer push or NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no soak, no e2e, no cpu baseline")
@@ -268,7 +269,7 @@ def main():
     uid = tk.broadcast_unique_id() if P > 1 else None
     stream = torch.cuda.Stream()
     ctx = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, nranks=P, rank=rank, group_size=n, seed=2010_10458,
-                     step4=a.step4, levels_per_pass=a.levels, uid=uid, stream=stream, device=local)
+                     step4=a.step4, levels_per_pass=a.levels, uid=uid, stream=stream, device=local, ag_mode=a.ag_mode)
     L, k = ctx.seg_len, ctx.k
     log("ctx up")
     # inputs: a fresh seeded N(0,1) gradient for every warm-up / timed / profiled step, generated on
@@ -400,6 +401,7 @@ def main():
                 "dtype": "f32", "data": "synthetic",
                 "config": {"workload": workload_name(a, P), "d": a.d, "rho": a.rho, "k": k, "n_iters": a.n_iters,
                            "P": P, "group_size": n, "step4": a.step4 if n > 1 else None, "dist": a.dist,
+                           "allgather": (a.ag_mode if n == 1 and P > 1 else None),
                            "levels_per_pass": a.levels or 4, "input_buffers": nbuf,
                            "inputs": "fresh seeded N(0,1) gradient per step (torch CUDA generator, pre-generated in "
                                      "HBM); residual carried from r=0 at step 0; timed steps W..W+K-1",

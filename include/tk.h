@@ -54,6 +54,10 @@ typedef enum tk_status {
 
 enum { TK_RAND_SEEDED = 0, TK_RAND_FIRST = 1 };   /* Alg. 1 l.27 window start (Q10)           */
 enum { TK_STEP4_DENSE = 0, TK_STEP4_SPARSE = 1 }; /* HiTopKComm step 4: Alg. 2 l.21-23 vs Eq.10*/
+enum { TK_AG_PUSH = 0, TK_AG_NCCL = 1 };          /* flat sparse all-gather (A9):
+                                                     PUSH = the compression writes its pairs into
+                                                     every peer's buffer over NVLink (P <= 8);
+                                                     NCCL = ncclAllGather after the compression */
 enum { TK_RS_ORDERED = 0, TK_RS_NCCL = 1 };       /* HiTopKComm step 1 reduce-scatter (Q20):
                                                      ORDERED = ascending-row-rank fp32 sum read over
                                                      NVLink peer pointers inside the EF kernel
@@ -79,6 +83,7 @@ typedef struct tk_config {
                               over the whole vector up to 2.  Result bits do not depend on it.  */
   int32_t device;          /* CUDA device ordinal to use (-1 = current)                        */
   uint32_t rs_mode;        /* HiTopKComm step-1 mode (TK_RS_ORDERED or TK_RS_NCCL)             */
+  uint32_t ag_mode;        /* flat all-gather mode (TK_AG_PUSH or TK_AG_NCCL)                  */
 } tk_config;
 
 /* Snapshot of the last compression's MSTopK control block (for parity checks). */
@@ -102,7 +107,7 @@ typedef struct tk_stats {
                               the first count pass (an exact shortcut)          */
   uint32_t n_compacted;    /* entries the first count pass kept (when compacted)                */
   uint32_t n_phases;       /* phase boundaries recorded in phase_ns                             */
-  uint64_t phase_ns[8];    /* device %globaltimer (ns) at k_compress's phase boundaries (CTA 0,
+  uint64_t phase_ns[12];   /* device %globaltimer (ns) at k_compress's phase boundaries (CTA 0,
                               after each grid barrier): start, stats, each count pass, prefix,
                               end of selection                                                 */
 } tk_stats;

@@ -38,7 +38,8 @@ class _Config(ctypes.Structure):
                 ("n_iters", ctypes.c_uint32), ("nranks", ctypes.c_uint32), ("rank", ctypes.c_uint32),
                 ("group_size", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("rand_mode", ctypes.c_uint32),
                 ("error_feedback", ctypes.c_uint32), ("step4", ctypes.c_uint32),
-                ("levels_per_pass", ctypes.c_uint32), ("device", ctypes.c_int32), ("rs_mode", ctypes.c_uint32)]
+                ("levels_per_pass", ctypes.c_uint32), ("device", ctypes.c_int32), ("rs_mode", ctypes.c_uint32),
+                ("ag_mode", ctypes.c_uint32)]
 
 
 class _Stats(ctypes.Structure):
@@ -52,7 +53,7 @@ class _Stats(ctypes.Structure):
                 ("len2", ctypes.c_uint64), ("rand_start", ctypes.c_uint64), ("step", ctypes.c_uint64),
                 ("nonfinite", ctypes.c_uint32), ("compacted", ctypes.c_uint32), ("n_compacted", ctypes.c_uint32),
                 ("n_phases", ctypes.c_uint32),
-                ("phase_ns", ctypes.c_uint64 * 8)]
+                ("phase_ns", ctypes.c_uint64 * 12)]
 
 
 # Every symbol include/tk.h declares (checked by tests/test_abi.py).
@@ -194,7 +195,7 @@ class Context:
     def __init__(self, d: int, rho: float = 0.001, n_iters: int = 10, *, k: int = 0, nranks: int = 1, rank: int = 0,
                  group_size: int = 1, seed: int = 0, rand_mode: str = "seeded", error_feedback: bool = True,
                  step4: str = "dense", levels_per_pass: int = 0, device: int | None = None, uid: bytes | None = None,
-                 stream: torch.cuda.Stream | None = None, rs_mode: str = "ordered"):
+                 stream: torch.cuda.Stream | None = None, rs_mode: str = "ordered", ag_mode: str = "push"):
         if not torch.cuda.is_available():
             raise RuntimeError("libtk needs a CUDA device (B200, sm_100a); there is no CPU fallback")
         dev = torch.cuda.current_device() if device is None else int(device)
@@ -204,7 +205,7 @@ class Context:
                       group_size=int(group_size), seed=int(seed) & ((1 << 64) - 1),
                       rand_mode={"seeded": 0, "first": 1}[rand_mode], error_feedback=1 if error_feedback else 0,
                       step4={"dense": 0, "sparse": 1}[step4], levels_per_pass=int(levels_per_pass), device=dev,
-                      rs_mode={"ordered": 0, "nccl": 1}[rs_mode])
+                      rs_mode={"ordered": 0, "nccl": 1}[rs_mode], ag_mode={"push": 0, "nccl": 1}[ag_mode])
         self._ctx = ctypes.c_void_p()
         if nranks > 1 and uid is None:
             raise ValueError("nranks > 1 needs the NCCL unique id (broadcast_unique_id())")

@@ -58,6 +58,9 @@ struct tk_ctx {
   float* sym_g = nullptr;             // HiTopKComm ordered RS: this GPU's peer-visible gradient [d]
   float* peer_g[8] = {nullptr};       // row peers' sym_g (IPC-opened; [row_pos] = sym_g)
   int32_t* sync_buf = nullptr;        // 4-byte buffer of the row barrier all-reduce
+  ulonglong2* pg = nullptr;           // TK_AG_PUSH: [2][P][k] tagged packets (double-buffered)
+  ulonglong2* peer_pg[8] = {nullptr}; // every rank's pg (IPC-opened; [rank] = pg)
+  uint32_t push_seq = 0;              // completed pushed steps (the packets' tag is push_seq + 1)
   uint64_t step = 0;
   uint64_t launches = 0;
   uint32_t nonfinite_sticky = 0;
@@ -150,7 +153,7 @@ int peer_sources(const tk_ctx* c) { return (c->n > 1 && c->cfg.rs_mode == TK_RS_
 // cooperative launch of k_compress.  With peers != nullptr the gradient is the ordered sum of the
 // np peer segments (HiTopKComm step 1).
 tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, float* val, const Peers* peers = nullptr,
-                        int np = 0) {
+                        int np = 0, const PushOut* push = nullptr) {
   const bool ef = c->cfg.error_feedback != 0;
   Fused f;
   memset(&f, 0, sizeof(f));
@@ -170,6 +173,7 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.cp = c->cp;
   f.idx_out = idx;
   f.val_out = val;
+  if (push) f.push = *push;
   f.c = c->ctrl;
   f.step = c->step;
   f.n_iters = c->cfg.n_iters;
@@ -185,14 +189,17 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   return TK_OK;
 }
 
-// Rank-ordered decompression of nchunks chunks of kk pairs into out[0, len).
-tk_status decompress_impl(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, uint64_t kk, uint64_t len,
-                          float* out) {
+// Rank-ordered decompression of nchunks chunks of kk pairs into out[0, len), from plain chunks or
+// (fused all-gather) from tagged packets, optionally re-emitting the pairs in the plain layout.
+template <class Src>
+tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t kk, uint64_t len, float* out,
+                          uint32_t* plain_out = nullptr) {
   const uint32_t nt = (uint32_t)((len + TILE - 1) / TILE);
   const uint32_t max_cta = c->sms * c->occ_dec;
   const uint32_t per = (nt + max_cta - 1) / max_cta;
   const uint32_t grid = (nt + per - 1) / per;
-  k_decompress<<<grid, THREADS, sizeof(uint32_t) * nchunks, c->stream>>>(gathered, nchunks, kk, len, nt, per, out);
+  k_decompress<Src><<<grid, THREADS, sizeof(uint32_t) * nchunks, c->stream>>>(src, nchunks, kk, len, nt, per, out,
+                                                                               plain_out);
   TK_TRY(check_launch(c, "k_decompress"));
   mark(c, TK_STAGE_DECOMPRESS);
   return TK_OK;
@@ -216,7 +223,7 @@ tk_status plan_launches(tk_ctx* c) {
   const void* kern = compress_kernel(c->cfg.error_feedback != 0, peer_sources(c));
   if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count");
   TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0));
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o7, k_decompress, THREADS, 64 * sizeof(uint32_t)));
+  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o7, k_decompress<PlainChunks>, THREADS, 64 * sizeof(uint32_t)));
   if (occ < 1) return fail(c, TK_ERR_CUDA, "k_compress cannot be resident");
   c->occ_dec = (uint32_t)std::max(1, o7);
   const uint64_t L = c->L;
@@ -243,37 +250,56 @@ tk_status plan_launches(tk_ctx* c) {
   return TK_OK;
 }
 
-// HiTopKComm ordered reduce-scatter: every GPU exposes a gradient buffer to its row peers through
-// CUDA IPC; the 64-byte handles are exchanged with an all-gather on the row communicator.
-tk_status open_row_peers(tk_ctx* c) {
-  TK_TRY(dev_alloc(c, &c->sym_g, c->d));
-  TK_TRY(dev_alloc(c, &c->sync_buf, 1));
-  TK_CUDA(c, cudaMemset(c->sync_buf, 0, sizeof(int32_t)));
+// Map `mine` (a cudaMalloc'd buffer) of every rank of `comm` into this process through CUDA IPC:
+// the 64-byte handles are exchanged with an NCCL all-gather; peers[me] = mine.
+tk_status exchange_ipc(tk_ctx* c, ncclComm_t comm, uint32_t nr, uint32_t me, void* mine_ptr, void** peers) {
   cudaIpcMemHandle_t mine;
-  TK_CUDA(c, cudaIpcGetMemHandle(&mine, c->sym_g));
+  TK_CUDA(c, cudaIpcGetMemHandle(&mine, mine_ptr));
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   char* dev = nullptr;
-  TK_TRY(dev_alloc(c, &dev, 64 * (size_t)(c->n + 1)));
+  TK_TRY(dev_alloc(c, &dev, 64 * (size_t)(nr + 1)));
   TK_CUDA(c, cudaMemcpy(dev, &mine, 64, cudaMemcpyHostToDevice));
-  ncclResult_t r = ncclAllGather(dev, dev + 64, 64, ncclChar, c->row, c->stream);
+  ncclResult_t r = ncclAllGather(dev, dev + 64, 64, ncclChar, comm, c->stream);
   if (r != ncclSuccess) {
     cudaFree(dev);
     return fail(c, TK_ERR_NCCL, "handle all-gather: %s", ncclGetErrorString(r));
   }
-  std::vector<cudaIpcMemHandle_t> all(c->n);
+  std::vector<cudaIpcMemHandle_t> all(nr);
   cudaError_t e = cudaStreamSynchronize(c->stream);
-  if (e == cudaSuccess) e = cudaMemcpy(all.data(), dev + 64, 64 * (size_t)c->n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(all.data(), dev + 64, 64 * (size_t)nr, cudaMemcpyDeviceToHost);
   cudaFree(dev);
   if (e != cudaSuccess) return fail(c, TK_ERR_CUDA, "handle exchange: %s", cudaGetErrorString(e));
-  for (uint32_t q = 0; q < c->n; ++q) {
-    if (q == c->row_pos) {
-      c->peer_g[q] = c->sym_g;
+  for (uint32_t q = 0; q < nr; ++q) {
+    if (q == me) {
+      peers[q] = mine_ptr;
       continue;
     }
-    void* p = nullptr;
-    TK_CUDA(c, cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess));
-    c->peer_g[q] = static_cast<float*>(p);
+    TK_CUDA(c, cudaIpcOpenMemHandle(&peers[q], all[q], cudaIpcMemLazyEnablePeerAccess));
   }
+  return TK_OK;
+}
+
+// HiTopKComm ordered reduce-scatter: every GPU exposes a gradient buffer to its row peers.
+tk_status open_row_peers(tk_ctx* c) {
+  TK_TRY(dev_alloc(c, &c->sym_g, c->d));
+  TK_TRY(dev_alloc(c, &c->sync_buf, 1));
+  TK_CUDA(c, cudaMemset(c->sync_buf, 0, sizeof(int32_t)));
+  void* peers[8] = {nullptr};
+  TK_TRY(exchange_ipc(c, c->row, c->n, c->row_pos, c->sym_g, peers));
+  for (uint32_t q = 0; q < c->n; ++q) c->peer_g[q] = static_cast<float*>(peers[q]);
+  return TK_OK;
+}
+
+// Flat fused all-gather (TK_AG_PUSH): every rank exposes a double-buffered buffer of tagged
+// packets [2][P][k] (16 B per pair, zeroed: tag 0 is never a step's tag); the compression writes
+// its pairs straight into its chunk on every peer over NVLink (see PushOut).
+tk_status open_push_peers(tk_ctx* c) {
+  const size_t n = 2 * (size_t)c->P * c->k;
+  TK_TRY(dev_alloc(c, &c->pg, n));
+  TK_CUDA(c, cudaMemset(c->pg, 0, sizeof(ulonglong2) * n));
+  void* peers[8] = {nullptr};
+  TK_TRY(exchange_ipc(c, c->world, c->P, c->rank, c->pg, peers));
+  for (uint32_t q = 0; q < c->P; ++q) c->peer_pg[q] = static_cast<ulonglong2*>(peers[q]);
   return TK_OK;
 }
 
@@ -290,6 +316,9 @@ void free_all(tk_ctx* c) {
   }
   for (uint32_t q = 0; q < 8; ++q)
     if (c->peer_g[q] && c->peer_g[q] != c->sym_g) cudaIpcCloseMemHandle(c->peer_g[q]);
+  for (uint32_t q = 0; q < 8; ++q)
+    if (c->peer_pg[q] && c->peer_pg[q] != c->pg) cudaIpcCloseMemHandle(c->peer_pg[q]);
+  if (c->pg) cudaFree(c->pg);
   if (c->sym_g) cudaFree(c->sym_g);
   if (c->sync_buf) cudaFree(c->sync_buf);
   if (c->row) ncclCommDestroy(c->row);
@@ -325,13 +354,16 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if (k.k == 0 && (!(k.rho > 0.0) || k.rho > 1.0)) return TK_ERR_INVALID_ARG;
   if (k.n_iters < 1 || k.n_iters > (uint32_t)NMAX) return TK_ERR_INVALID_ARG;
   if (k.nranks < 1 || k.rank >= k.nranks) return TK_ERR_INVALID_ARG;
-  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 8 || k.rs_mode > 1) return TK_ERR_INVALID_ARG;
+  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 8 || k.rs_mode > 1 ||
+      k.ag_mode > 1)
+    return TK_ERR_INVALID_ARG;
   const uint32_t n = k.group_size == 0 ? 1 : k.group_size;
   if (k.nranks % n != 0) return TK_ERR_CONFIG;
   if (k.d % n != 0) return TK_ERR_CONFIG;
   if (n > 1 && (k.d / n) % 4 != 0) return TK_ERR_CONFIG;  // segments start 16-byte aligned (128-bit access)
   if (k.nranks > 1 && !uid) return TK_ERR_CONFIG;
   if (n > 1 && k.rs_mode == TK_RS_ORDERED && n != 2 && n != 4 && n != 8) return TK_ERR_CONFIG;
+  if (n == 1 && k.ag_mode == TK_AG_PUSH && k.nranks > 8) return TK_ERR_CONFIG;
   const uint64_t L = k.d / n;
   uint64_t kk = k.k;
   if (kk == 0) kk = tk_k(L, k.rho);
@@ -398,6 +430,8 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
           ncclCommSplit(c->world, (int)(c->rank % n), (int)c->rank, &c->col, nullptr) != ncclSuccess)
         return bail(TK_ERR_NCCL);
       if (k.rs_mode == TK_RS_ORDERED && (s = open_row_peers(c)) != TK_OK) return bail(s);
+    } else if (k.ag_mode == TK_AG_PUSH) {
+      if ((s = open_push_peers(c)) != TK_OK) return bail(s);
     }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(TK_ERR_CUDA);
@@ -443,7 +477,7 @@ tk_status tk_decompress(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, f
   if (!aligned16(out)) return fail(c, TK_ERR_INVALID_ARG, "out must be 16-byte aligned");
   if (nchunks < 1 || nchunks > 4096) return fail(c, TK_ERR_INVALID_ARG, "nchunks must lie in [1, 4096]");
   const uint64_t len = (c->n == 1) ? c->d : c->L;
-  return decompress_impl(c, gathered, nchunks, c->k, len, out);
+  return decompress_impl(c, PlainChunks{gathered, c->k}, nchunks, c->k, len, out);
 }
 
 tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gathered) {
@@ -459,10 +493,32 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
     // in-place all-gather -> rank-ordered decompress
     uint32_t* gat = gathered ? gathered : c->recv;
     uint32_t* mine = gat + (size_t)c->rank * 2 * c->k;
-    TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k)));
-    if (c->P > 1) TK_NCCL(c, ncclAllGather(mine, gat, 2 * c->k, ncclUint32, c->world, c->stream));
-    mark(c, TK_STAGE_ALLGATHER);
-    TK_TRY(decompress_impl(c, gat, c->P, c->k, c->d, out));
+    if (c->P > 1 && c->pg) {
+      // fused all-gather (TK_AG_PUSH): the compression selects into this rank's plain slot, then
+      // each CTA pushes its run of pairs as tagged packets into this rank's chunk on every GPU;
+      // the decompression consumes the packets as they land (waiting per packet on its tag) and
+      // re-emits the gathered pairs in the plain layout.  Double-buffered by step parity: a
+      // peer writes step s+2 into a buffer only after its step s+1 decompression consumed this
+      // rank's step s+1 packets, which this rank pushed after its step s decompression finished.
+      const uint32_t parity = c->push_seq & 1u;
+      const size_t stride = (size_t)c->P * c->k;
+      PushOut po;
+      memset(&po, 0, sizeof(po));
+      po.np = c->P;
+      po.me = c->rank;
+      po.tag = c->push_seq + 1;
+      for (uint32_t q = 0; q < c->P; ++q) po.slot[q] = c->peer_pg[q] + parity * stride + (size_t)c->rank * c->k;
+      TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k), nullptr, 0, &po));
+      c->push_seq++;
+      mark(c, TK_STAGE_ALLGATHER);
+      TaggedChunks src{c->pg + parity * stride, c->k, po.tag};
+      TK_TRY(decompress_impl(c, src, c->P, c->k, c->d, out, gat));
+    } else {
+      TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k)));
+      if (c->P > 1) TK_NCCL(c, ncclAllGather(mine, gat, 2 * c->k, ncclUint32, c->world, c->stream));
+      mark(c, TK_STAGE_ALLGATHER);
+      TK_TRY(decompress_impl(c, PlainChunks{gat, c->k}, c->P, c->k, c->d, out));
+    }
   } else {
     // HiTopKComm (Alg. 2).  The compressed segment goes straight into this GPU's slot (its node
     // index i = col_pos) of the column-gathered buffer.
@@ -497,7 +553,7 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
     if (c->cfg.step4 == TK_STEP4_DENSE) {
       // ... accumulated in group order into this GPU's segment, then step 4: dense intra-node
       // all-gather of the segments (Alg. 2 l.21-23), in place.
-      TK_TRY(decompress_impl(c, gat, c->m, c->k, c->L, my_seg));
+      TK_TRY(decompress_impl(c, PlainChunks{gat, c->k}, c->m, c->k, c->L, my_seg));
       TK_NCCL(c, ncclAllGather(my_seg, out, c->L, ncclFloat32, c->row, c->stream));
       mark(c, TK_STAGE_STEP4_ALLGATHER);
     } else {
@@ -506,7 +562,7 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
       TK_NCCL(c, ncclAllGather(gat, c->recv_row, (size_t)c->m * 2 * c->k, ncclUint32, c->row, c->stream));
       mark(c, TK_STAGE_STEP4_ALLGATHER);
       for (uint32_t j = 0; j < c->n; ++j)
-        TK_TRY(decompress_impl(c, c->recv_row + (size_t)j * c->m * 2 * c->k, c->m, c->k, c->L,
+        TK_TRY(decompress_impl(c, PlainChunks{c->recv_row + (size_t)j * c->m * 2 * c->k, c->k}, c->m, c->k, c->L,
                                out + (size_t)j * c->L));
     }
   }
@@ -573,8 +629,8 @@ tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
   st->nonfinite = c->nonfinite_sticky;
   st->compacted = h.cap_ok;
   st->n_compacted = h.n_compacted;
-  st->n_phases = std::min<uint32_t>(8, h.n_phase);
-  for (int i = 0; i < 8; ++i) st->phase_ns[i] = h.phase_ns[i];
+  st->n_phases = std::min<uint32_t>(12, h.n_phase);
+  for (int i = 0; i < 12; ++i) st->phase_ns[i] = h.phase_ns[i];
   if (c->nonfinite_sticky) return fail(c, TK_ERR_NONFINITE, "non-finite value in acc (precondition, Q24)");
   return TK_OK;
 }

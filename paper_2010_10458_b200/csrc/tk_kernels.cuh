@@ -53,7 +53,7 @@ struct Ctrl {
   double thres_log[NMAX];
   uint32_t key_log[NMAX];
   uint32_t nnz_log[NMAX];
-  uint64_t phase_ns[8];  // %globaltimer at the phase boundaries of the last k_compress (CTA 0)
+  uint64_t phase_ns[12];  // %globaltimer at the phase boundaries of the last k_compress (CTA 0)
   uint32_t n_phase;
   uint32_t n_compacted;  // entries kept by the first count pass (all warps)
   uint32_t cand_tree;    // the candidates form a complete subtree (walked by index in replay)
@@ -81,6 +81,60 @@ struct Compact {
   uint32_t* bits;
   uint32_t* cnt;
   uint32_t C;  // capacity per warp (multiple of 4)
+};
+
+// TK_AG_PUSH (fused all-gather): slot[q] = this rank's chunk of peer q's gathered buffer (q == me:
+// the local one).  A pair travels as one 16-byte packet of two 8-byte words {idx, tag} and
+// {val, tag}; tag = the step's sequence number.  Each 8-byte word is written and read as one
+// single-copy-atomic access, so a reader that sees both tags equal to the step's sequence has the
+// pair -- no fence, no flag, no counter (the "tag in every word" protocol).
+struct PushOut {
+  ulonglong2* slot[8];
+  uint32_t np, me, tag;
+};
+
+__device__ __forceinline__ void st_ll(ulonglong2* p, uint32_t i, uint32_t v, uint32_t tag) {
+  const uint64_t a = (uint64_t)i | ((uint64_t)tag << 32), b = (uint64_t)v | ((uint64_t)tag << 32);
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ ulonglong2 ld_ll(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
+// chunked pair sources of the decompression
+struct PlainChunks {  // [nchunks][idx k | val k] u32
+  const uint32_t* g;
+  uint64_t k;
+  __device__ __forceinline__ uint32_t idx(uint32_t p, uint32_t j) const { return __ldg(g + (size_t)p * 2 * k + j); }
+  __device__ __forceinline__ void get(uint32_t p, uint32_t j, uint32_t& i, float& v) const {
+    i = __ldg(g + (size_t)p * 2 * k + j);
+    v = __uint_as_float(__ldg(g + (size_t)p * 2 * k + k + j));
+  }
+};
+
+struct TaggedChunks {  // [nchunks][k] tagged packets, written by the peers during this step
+  const ulonglong2* g;
+  uint64_t k;
+  uint32_t tag;
+  __device__ __forceinline__ void get(uint32_t p, uint32_t j, uint32_t& i, float& v) const {
+    const ulonglong2* a = g + (size_t)p * k + j;
+    ulonglong2 x = ld_ll(a);
+    while ((uint32_t)(x.x >> 32) != tag || (uint32_t)(x.y >> 32) != tag) {
+      __nanosleep(32);
+      x = ld_ll(a);
+    }
+    i = (uint32_t)x.x;
+    v = __uint_as_float((uint32_t)x.y);
+  }
+  __device__ __forceinline__ uint32_t idx(uint32_t p, uint32_t j) const {
+    uint32_t i;
+    float v;
+    get(p, j, i, v);
+    return i;
+  }
 };
 
 // ------------------------------------------------------------------------------------------
@@ -848,15 +902,13 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
         if (fc1 & (1u << e)) {
           const uint32_t after = (q2 > rnd) ? min(q2 - rnd, need) : 0u;
           const uint32_t pos = q1 + after;
-          idx_out[pos] = ii[e];
-          val_out[pos] = __uint_as_float(bb[e]);
+          { idx_out[pos] = ii[e]; val_out[pos] = __uint_as_float(bb[e]); }
           if (r_zero) r_zero[ii[e]] = 0.0f;
           ++q1;
         } else if (fc2 & (1u << e)) {
           if (q2 >= rnd && q2 < rnd + need) {
             const uint32_t pos = q1 + (q2 - rnd);
-            idx_out[pos] = ii[e];
-            val_out[pos] = __uint_as_float(bb[e]);
+            { idx_out[pos] = ii[e]; val_out[pos] = __uint_as_float(bb[e]); }
             if (r_zero) r_zero[ii[e]] = 0.0f;
           }
           ++q2;
@@ -900,15 +952,13 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
         if (fc1 & (1u << e)) {
           const uint32_t after = (q2 > rnd) ? min(q2 - rnd, need) : 0u;
           const uint32_t pos = q1 + after;
-          idx_out[pos] = i;
-          val_out[pos] = __uint_as_float(__ldg(a32 + i));
+          { idx_out[pos] = i; val_out[pos] = __uint_as_float(__ldg(a32 + i)); }
           if (r_zero) r_zero[i] = 0.0f;
           ++q1;
         } else {
           if (q2 >= rnd && q2 < rnd + need) {
             const uint32_t pos = q1 + (q2 - rnd);
-            idx_out[pos] = i;
-            val_out[pos] = __uint_as_float(__ldg(a32 + i));
+            { idx_out[pos] = i; val_out[pos] = __uint_as_float(__ldg(a32 + i)); }
             if (r_zero) r_zero[i] = 0.0f;
           }
           ++q2;
@@ -970,6 +1020,7 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
 
 struct Fused {
   SearchParams sp;
+  PushOut push;              // np == 0: no fused all-gather
   const float* g;            // gradient (flat) - unused when the peers supply it
   Peers pr;                  // HiTopKComm ordered reduce-scatter sources
   float* r;                  // residual in, acc / r' out (EF); nullptr without EF
@@ -1036,9 +1087,9 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)
   int nph = 0;
   auto stamp = [&]() {
-    if (tid == 0 && nph < 8) sc.phase_ns[nph] = globaltimer();
+    if (tid == 0 && nph < 12) sc.phase_ns[nph] = globaltimer();
     ++nph;
-    sc.n_phase = (uint32_t)min(nph, 8);
+    sc.n_phase = (uint32_t)min(nph, 12);
   };
   stamp();
   if (blockIdx.x == 0) {
@@ -1177,6 +1228,24 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   // ---- A7-A8: selection, compaction, residual write-back ----
   select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, f.idx_out, f.val_out, EF ? f.r : nullptr, f.cp);
   stamp();
+  if (f.push.np > 0) {
+    // Fused all-gather.  The kept elements of this CTA occupy ONE contiguous run of output
+    // positions: pos = #class1 before + clamp(#class2 before - rand, 0, need) is monotone and
+    // steps by one per kept element.  Copy the run (written locally above) as tagged packets to
+    // this rank's chunk on every GPU (peers over NVLink, coalesced 16-byte stores).
+    uint32_t t1 = 0, t2 = 0;
+    for (int w = 0; w < WARPS; ++w) { t1 += s_w[0][w]; t2 += s_w[1][w]; }
+    const uint32_t rnd = sc.rand, need = sc.need;
+    auto kept2 = [&](uint32_t q2) { return q2 > rnd ? min(q2 - rnd, need) : 0u; };
+    const uint32_t p0 = s_base[0] + kept2(s_base[1]);
+    const uint32_t p1 = s_base[0] + t1 + kept2(s_base[1] + t2);
+    __syncthreads();
+    for (uint32_t pos = p0 + tid; pos < p1; pos += THREADS) {
+      const uint32_t i = __ldcg(f.idx_out + pos);
+      const uint32_t v = __ldcg(reinterpret_cast<const uint32_t*>(f.val_out) + pos);
+      for (uint32_t q = 0; q < f.push.np; ++q) st_ll(f.push.slot[q] + pos, i, v, f.push.tag);
+    }
+  }
   if (blockIdx.x == 0) {
     uint32_t tn = 0;
     for (uint32_t b = tid; b < gridDim.x; b += THREADS) tn += __ldcg(f.cta_cls + 2 * gridDim.x + b);
@@ -1201,14 +1270,15 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
 // (chunks are ascending), found once per CTA by a warp-cooperative 32-ary search.  No global
 // atomics, no read-modify-write of out.  HBM: 4 B/elem write + 8 B per gathered pair.
 
-// first j in [0, n) with a[j] >= target (n if none); all lanes of the warp participate
-__device__ uint32_t warp_lower_bound(const uint32_t* a, uint32_t n, uint32_t target) {
+// first j in [0, n) with src.idx(p, j) >= target (n if none); all lanes of the warp participate
+template <class Src>
+__device__ uint32_t warp_lower_bound(const Src& src, uint32_t p, uint32_t n, uint32_t target) {
   const int lane = threadIdx.x & 31;
   uint32_t lo = 0, hi = n;
   while (hi - lo > 32) {
     const uint32_t step = (hi - lo + 31) / 32;
     const uint32_t pos = lo + lane * step;
-    const uint32_t v = pos < hi ? __ldg(a + pos) : 0xFFFFFFFFu;
+    const uint32_t v = pos < hi ? src.idx(p, pos) : 0xFFFFFFFFu;
     const uint32_t m = __ballot_sync(0xffffffffu, v >= target);
     const uint32_t f = m ? (uint32_t)(__ffs(m) - 1) : 32u;
     if (f == 0) return lo;
@@ -1218,22 +1288,31 @@ __device__ uint32_t warp_lower_bound(const uint32_t* a, uint32_t n, uint32_t tar
     hi = nhi;
   }
   const uint32_t pos = lo + lane;
-  const uint32_t v = pos < hi ? __ldg(a + pos) : 0xFFFFFFFFu;
+  const uint32_t v = pos < hi ? src.idx(p, pos) : 0xFFFFFFFFu;
   const uint32_t m = __ballot_sync(0xffffffffu, pos < hi && v >= target);
   return m ? lo + (uint32_t)(__ffs(m) - 1) : hi;
 }
 
-__global__ void __launch_bounds__(THREADS) k_decompress(const uint32_t* __restrict__ gathered, uint32_t nchunks,
-                                                        uint64_t k, uint64_t n, uint32_t ntiles, uint32_t tiles_per_cta,
-                                                        float* __restrict__ out) {
+// plain_out (optional): the consumed pairs re-emitted in the plain [nchunks][idx k | val k]
+// layout (each pair lies in exactly one tile, so each is written exactly once)
+template <class Src>
+__global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t nchunks, uint64_t k, uint64_t n,
+                                                        uint32_t ntiles, uint32_t tiles_per_cta,
+                                                        float* __restrict__ out, uint32_t* __restrict__ plain_out) {
   __shared__ __align__(16) float s_tile[TILE];
   extern __shared__ uint32_t s_cur[];  // [nchunks] per-rank cursors
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t t0 = blockIdx.x * tiles_per_cta;
   const uint32_t t1 = min(ntiles, t0 + tiles_per_cta);
   if (t0 >= t1) return;
+  auto emit = [&](uint32_t p, uint32_t j, uint32_t i, float v) {
+    if (plain_out) {
+      plain_out[(size_t)p * 2 * k + j] = i;
+      plain_out[(size_t)p * 2 * k + k + j] = __float_as_uint(v);
+    }
+  };
   for (uint32_t p = warp; p < nchunks; p += WARPS) {
-    const uint32_t j = warp_lower_bound(gathered + (size_t)p * 2 * k, (uint32_t)k, t0 * TILE);
+    const uint32_t j = warp_lower_bound(src, p, (uint32_t)k, t0 * TILE);
     if (lane == 0) s_cur[p] = j;
   }
   __syncthreads();
@@ -1244,23 +1323,21 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const uint32_t* __restri
     uint32_t pi = NO_INDEX, cnt = 0, cur = 0;
     float pv = 0.0f;
     if (warp < (int)nchunks) {
-      const uint32_t* ch = gathered + (size_t)warp * 2 * k;
       cur = s_cur[warp];
       const uint32_t j = cur + lane;
-      if (j < k) {
-        pi = __ldg(ch + j);
-        pv = __uint_as_float(__ldg(ch + k + j));
-      }
+      if (j < k) src.get(warp, j, pi, pv);
       cnt = __popc(__ballot_sync(0xffffffffu, pi < thi));
     }
     for (int q = threadIdx.x; q < TILE / 4; q += THREADS) s4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     for (uint32_t p = 0; p < nchunks; ++p) {
       if ((uint32_t)warp == (p & (WARPS - 1))) {
-        const uint32_t* ch = gathered + (size_t)p * 2 * k;
         uint32_t c0;
         if (p < WARPS) {
-          if (pi < thi) s_tile[pi - tlo] = __fadd_rn(s_tile[pi - tlo], pv);
+          if (pi < thi) {
+            s_tile[pi - tlo] = __fadd_rn(s_tile[pi - tlo], pv);
+            emit(p, cur + lane, pi, pv);
+          }
           c0 = cur + cnt;
         } else {
           c0 = s_cur[p];
@@ -1268,9 +1345,14 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const uint32_t* __restri
         if (p >= WARPS || cnt == 32) {  // more pairs of this rank in this tile
           for (;;) {
             const uint32_t j = c0 + lane;
-            const uint32_t i = j < k ? __ldg(ch + j) : NO_INDEX;
+            uint32_t i = NO_INDEX;
+            float v = 0.0f;
+            if (j < k) src.get(p, j, i, v);
             const bool in = i < thi;
-            if (in) s_tile[i - tlo] = __fadd_rn(s_tile[i - tlo], __uint_as_float(__ldg(ch + k + j)));
+            if (in) {
+              s_tile[i - tlo] = __fadd_rn(s_tile[i - tlo], v);
+              emit(p, j, i, v);
+            }
             const uint32_t m = __popc(__ballot_sync(0xffffffffu, in));
             c0 += m;
             if (m < 32) break;

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--dist", default="G")
     ap.add_argument("--step4", default="dense")
     ap.add_argument("--rs-mode", default="ordered")
+    ap.add_argument("--ag-mode", default="push")
     ap.add_argument("--zero-copy", action="store_true", help="write g into the context's input buffer")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
@@ -47,7 +48,7 @@ def main():
     log("uid ok")
     n = a.group_size
     ctx = tk.Context(a.dim, rho=a.rho, n_iters=a.n_iters, nranks=ws, rank=rank, group_size=n, seed=99, uid=uid,
-                     step4=a.step4, rs_mode=a.rs_mode, device=local)
+                     step4=a.step4, rs_mode=a.rs_mode, ag_mode=a.ag_mode, device=local)
     L, k = ctx.seg_len, ctx.k
     log("ctx ok", L, k)
     chunks = ws if n == 1 else ws // n

@@ -53,8 +53,9 @@ def _run(P, tmp_path, **kw):
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_flat_sparse_allgather(P, tmp_path):
-    _run(P, tmp_path, dim=1_000_003, rho=0.001, steps=3)
+@pytest.mark.parametrize("ag", ["push", "nccl"])
+def test_flat_sparse_allgather(P, ag, tmp_path):
+    _run(P, tmp_path, dim=1_000_003, rho=0.001, steps=3, ag_mode=ag)
 
 
 @pytest.mark.parametrize("P", [2, 4, 8])
