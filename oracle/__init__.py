@@ -6,14 +6,14 @@ written from PAPER.md and the readings listed in DESIGN.md.  Importable only fro
 ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (``cpu_baseline`` and
 ``--impl reference``).  Shares no code with ``paper_2010_10458_b200``.
 """
-from .mstopk import (RAND_FIRST, RAND_SEEDED, CompressResult, MSTopKResult, ceil_f32_bits, compress,
-                     exact_topk, k_from_density, magnitudes, mstopk, pairwise_sum_f64)
+from .mstopk import (RAND_FIRST, RAND_SEEDED, CompressResult, ExactResult, MSTopKResult, ceil_f32_bits,
+                     compress, exact_select, exact_topk, k_from_density, magnitudes, mstopk, pairwise_sum_f64)
 from .aggregate import (FlatResult, HiTopKResult, allgather, decompress, flat_step, hitopk_step, pack,
                         reduce_scatter_ordered)
 from .rng import splitmix64, window_hash
 
 __all__ = [
-    "RAND_FIRST", "RAND_SEEDED", "CompressResult", "MSTopKResult", "ceil_f32_bits", "compress", "exact_topk",
+    "RAND_FIRST", "RAND_SEEDED", "CompressResult", "ExactResult", "MSTopKResult", "exact_select", "ceil_f32_bits", "compress", "exact_topk",
     "k_from_density", "magnitudes", "mstopk", "pairwise_sum_f64", "FlatResult", "HiTopKResult", "allgather",
     "decompress", "flat_step", "hitopk_step", "pack", "reduce_scatter_ordered", "splitmix64", "window_hash",
 ]

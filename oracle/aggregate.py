@@ -43,14 +43,16 @@ class FlatResult:
 
 
 def flat_step(grads: list, residuals: list, rho: float, n_iters: int, *, seed: int = 0, step: int = 0,
-              rand_mode: int = RAND_SEEDED, error_feedback: bool = True, k: int | None = None) -> FlatResult:
+              rand_mode: int = RAND_SEEDED, error_feedback: bool = True, k: int | None = None,
+              selector: str = "mstopk") -> FlatResult:
     """NaiveAG TopK-SGD aggregation (§5.3) with error feedback (BJ):
     compress on every rank, all-gather the packed pairs, decompress in rank order."""
     P = len(grads)
     d = grads[0].shape[0]
     kk = k if k is not None else k_from_density(d, rho)
     per = [compress(grads[p], residuals[p] if error_feedback else None, kk, n_iters, seed=seed, step=step,
-                    rank=p, rand_mode=rand_mode, error_feedback=error_feedback) for p in range(P)]
+                    rank=p, rand_mode=rand_mode, error_feedback=error_feedback, selector=selector)
+           for p in range(P)]
     gathered = allgather([pack(c.sel.idx, c.sel.val) for c in per])
     return FlatResult(out=decompress(gathered, P, kk, d), gathered=gathered, per_rank=per)
 
@@ -76,7 +78,8 @@ class HiTopKResult:
 
 
 def hitopk_step(grads: list, residuals: list, m: int, n: int, rho: float, n_iters: int, *, seed: int = 0,
-                step: int = 0, rand_mode: int = RAND_SEEDED, error_feedback: bool = True) -> HiTopKResult:
+                step: int = 0, rand_mode: int = RAND_SEEDED, error_feedback: bool = True,
+                selector: str = "mstopk") -> HiTopKResult:
     """HiTopKComm (Alg. 2) on m x n GPUs; world rank = i*n + j.
     residuals[rank] is the segment residual in R^{d/n} (Q22)."""
     P = m * n
@@ -92,7 +95,8 @@ def hitopk_step(grads: list, residuals: list, m: int, n: int, rho: float, n_iter
             segs.append(reduce_scatter_ordered(grads, n, i, j))
     for rank in range(P):  # Alg. 2 l.6-8: MSTopK on every segment
         per.append(compress(segs[rank], residuals[rank] if error_feedback else None, kt, n_iters, seed=seed,
-                            step=step, rank=rank, rand_mode=rand_mode, error_feedback=error_feedback))
+                            step=step, rank=rank, rand_mode=rand_mode, error_feedback=error_feedback,
+                            selector=selector))
     col = []
     G = []
     for j in range(n):  # Alg. 2 l.11-14: column All-Gather among GPUs (0..m-1, j)

@@ -182,6 +182,26 @@ def exact_topk(x: np.ndarray, k: int):
 
 
 @dataclass
+class ExactResult:
+    """Exact top-k (Eq. 2) of one vector, plus the order statistic that decides it."""
+    idx: np.ndarray     # uint32[k], ascending
+    val: np.ndarray     # float32[k], signed acc values (Q12)
+    k: int
+    kth_bits: int       # bits(|x|) of the k-th largest magnitude (T)
+    k1: int             # #{i : bits(|x_i|) > T}   (all selected)
+    k2: int             # #{i : bits(|x_i|) >= T}  (the first k - k1 of the ties at T, by index, are selected)
+
+
+def exact_select(x: np.ndarray, k: int) -> ExactResult:
+    """exact_topk plus its k-th order statistic, read off the sorted magnitudes (definitions only)."""
+    idx, val = exact_topk(x, k)
+    bits = magnitudes(np.ascontiguousarray(x, dtype=np.float32)).view(np.uint32)
+    T = int(np.sort(bits)[::-1][k - 1])
+    return ExactResult(idx=idx, val=val, k=k, kth_bits=T, k1=int(np.count_nonzero(bits > T)),
+                       k2=int(np.count_nonzero(bits >= T)))
+
+
+@dataclass
 class CompressResult:
     sel: MSTopKResult
     acc: np.ndarray        # the vector MSTopK ran on (g + r with error feedback, else g)
@@ -190,15 +210,21 @@ class CompressResult:
 
 def compress(g: np.ndarray, r: np.ndarray | None, k: int, n_iters: int, *, seed: int = 0,
              step: int = 0, rank: int = 0, rand_mode: int = RAND_SEEDED,
-             error_feedback: bool = True) -> CompressResult:
+             error_feedback: bool = True, selector: str = "mstopk") -> CompressResult:
     """One rank's compression with error feedback (BJ north_star; Q14):
-    acc = fl32(g + r); (kappa, iota) = MSTopK(acc); r' = acc with the sent entries := +0.0."""
+    acc = fl32(g + r); (kappa, iota) = MSTopK(acc) -- or, with selector="exact", the exact top-k
+    of Eq. 2 (TopK-SGD; ties -> lower index, Q6); r' = acc with the sent entries := +0.0."""
     g = np.ascontiguousarray(g, dtype=np.float32)
     if error_feedback:
         acc = (g + np.ascontiguousarray(r, dtype=np.float32)).astype(np.float32)
     else:
         acc = g.copy()
-    sel = mstopk(acc, k, n_iters, seed=seed, step=step, rank=rank, rand_mode=rand_mode)
+    if selector == "exact":
+        sel = exact_select(acc, k)
+    elif selector == "mstopk":
+        sel = mstopk(acc, k, n_iters, seed=seed, step=step, rank=rank, rand_mode=rand_mode)
+    else:
+        raise ValueError(f"unknown selector {selector!r}")
     res = None
     if error_feedback:
         res = acc.copy()

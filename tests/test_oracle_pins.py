@@ -170,6 +170,51 @@ def test_exact_topk_matches_sort_on_seeded_vector():
         assert oracle.exact_topk(x, k)[0].tolist() == _brute_topk(xs, k)
 
 
+def test_exact_select_order_statistic_brute_force():
+    """T = bits of the k-th largest |x| (python sorted over the magnitudes), k1 = #> T < k <= k2 = #>= T,
+    every selected magnitude >= T, every unselected one <= T, ties at T taken by lowest index."""
+    for dist, d in [("G", 997), ("ties8", 1000), ("zero", 64), ("const", 33), ("spike", 100), ("L", 4096)]:
+        x = gradgen.gradient(d, dist, cfg=7)
+        mags = sorted((abs(float(v)) for v in x.tolist()), reverse=True)
+        for k in sorted({1, 2, d // 3 + 1, d - 1, d} - {0}):
+            e = oracle.exact_select(x, k)
+            assert float(np.abs(x[e.idx.astype(np.int64)]).min()) == mags[k - 1]
+            assert np.float32(mags[k - 1]).view(np.uint32) == e.kth_bits
+            assert e.k1 == sum(1 for m in mags if m > mags[k - 1]) and e.k1 < k <= e.k2
+            assert e.k2 == sum(1 for m in mags if m >= mags[k - 1])
+            ties = [i for i in range(d) if abs(float(x[i])) == mags[k - 1]]
+            sel = set(e.idx.tolist())
+            assert [i for i in ties if i in sel] == ties[:k - e.k1]
+
+
+def test_compress_exact_selector_error_feedback():
+    """selector="exact": idx = exact_topk(acc), r' + scatter(idx, val) == acc bitwise, acc = fl32(g + r)."""
+    d, k = 5000, 17
+    g = gradgen.gradient(d, "H", cfg=8)
+    r = gradgen.gradient(d, "G", cfg=9) * np.float32(0.01)
+    c = oracle.compress(g, r, k, 10, selector="exact")
+    assert np.array_equal(c.acc.view(np.uint32), (g + r).astype(np.float32).view(np.uint32))
+    assert c.sel.idx.tolist() == oracle.exact_topk(c.acc, k)[0].tolist()
+    back = c.residual.copy()
+    back[c.sel.idx.astype(np.int64)] += c.sel.val
+    assert np.array_equal(back.view(np.uint32), c.acc.view(np.uint32))
+    with pytest.raises(ValueError):
+        oracle.compress(g, r, k, 10, selector="sort")
+
+
+def test_exact_selector_density_one_flat_is_dense_sum():
+    """rho = 1 with the exact selector: every element is sent, so the flat step is the rank-ordered dense sum."""
+    d, P = 300, 3
+    gs = [gradgen.gradient(d, "G", cfg=11, rank=p) for p in range(P)]
+    rs = [np.zeros(d, np.float32) for _ in range(P)]
+    res = oracle.flat_step(gs, rs, 1.0, 5, selector="exact")
+    want = np.zeros(d, np.float32)
+    for p in range(P):
+        want = (want + gs[p]).astype(np.float32)
+    assert np.array_equal(res.out.view(np.uint32), want.view(np.uint32))
+    assert all(not np.any(c.residual) for c in res.per_rank)
+
+
 # ---------------------------------------------------------------- MSTopK invariants
 def _check_mstopk_invariants(x, k, N, res):
     a = np.abs(x).astype(np.float64)
@@ -320,6 +365,8 @@ def test_e4_hitopk_spec_example(golden):
         idx, val = oracle.exact_topk(v, 2)
         out[idx.astype(np.int64)] += val
     assert out.tolist() == g["out_exact_selector"]
+    res = oracle.hitopk_step(gs, rs, g["m"], g["n"], g["rho"], g["N"], selector="exact")
+    assert res.out.tolist() == g["out_exact_selector"]
 
 
 @pytest.mark.parametrize("m,n", [(2, 4), (4, 2), (1, 4), (2, 1)])
