@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--step4", default="dense", choices=["dense", "sparse"])
     ap.add_argument("--levels", type=int, default=0, help="bisection levels per count pass (0 = default)")
     ap.add_argument("--ag-mode", default="push", choices=["push", "nccl"], help="flat all-gather: fused peer push or NCCL")
+    ap.add_argument("--select", default="mstopk", choices=["mstopk", "exact"],
+                    help="selector: MSTopK (Alg. 1) or the exact top-k of Eq. 2 (SURVEY F1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no soak, no e2e, no cpu baseline")
@@ -61,6 +63,8 @@ def workload_name(a, P):
     if a.group_size > 1:
         return f"C4 HiTopKComm {P // a.group_size}x{a.group_size} d={a.d} rho={a.rho} N={a.n_iters}"
     tag = "C2" if a.d == 25_600_000 else ("C3" if a.d == 110_000_000 else "custom")
+    if a.select == "exact":
+        return f"{tag} exact top-k (Eq. 2) + flat sparse allgather d={a.d} rho={a.rho} EF P={P}"
     return f"{tag} flat sparse allgather d={a.d} rho={a.rho} N={a.n_iters} EF P={P}"
 
 
@@ -176,26 +180,26 @@ def sum_over_ranks(x, ws):
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle
-def time_oracle_step(d, rho, N, P, n, seed=1, dist="G"):
+def time_oracle_step(d, rho, N, P, n, seed=1, dist="G", selector="mstopk"):
     """One full simulated step of the oracle (all P ranks in one process); returns seconds."""
     import oracle
     gs = [gradgen.gradient(d, dist, cfg=2, rank=p, step=0) for p in range(P)]
     t0 = time.perf_counter()
     if n == 1:
         rs = [np.zeros(d, np.float32) for _ in range(P)]
-        oracle.flat_step(gs, rs, rho, N, seed=seed)
+        oracle.flat_step(gs, rs, rho, N, seed=seed, selector=selector)
     else:
         rs = [np.zeros(d // n, np.float32) for _ in range(P)]
-        oracle.hitopk_step(gs, rs, P // n, n, rho, N, seed=seed)
+        oracle.hitopk_step(gs, rs, P // n, n, rho, N, seed=seed, selector=selector)
     return time.perf_counter() - t0
 
 
 def cpu_baseline(a, P, budget_s=15.0):
     d_s = a.d
-    t = time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist)
+    t = time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist, selector=a.select)
     reps, total = 1, t
     while total < budget_s and reps < 30:
-        total += time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist)
+        total += time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist, selector=a.select)
         reps += 1
     return {"value": d_s * reps / total, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{reps} full single-rank oracle steps (numpy, 1 thread) at d={d_s}, rho={a.rho}, N={a.n_iters}, "
@@ -209,8 +213,8 @@ def run_reference(a, ws, rank, emit):
     n = a.group_size
     d_s = max(n * 4096, (min(a.d, 25_600_000 // P) // n) * n)  # bounded sample of the workload per step
     for _ in range(a.warmup):
-        time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist)
-    ts = [time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist) for _ in range(a.steps)]
+        time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist, selector=a.select)
+    ts = [time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist, selector=a.select) for _ in range(a.steps)]
     t = sum(ts) / len(ts)
     val = P * d_s / t
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
@@ -269,7 +273,8 @@ def main():
     uid = tk.broadcast_unique_id() if P > 1 else None
     stream = torch.cuda.Stream()
     ctx = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, nranks=P, rank=rank, group_size=n, seed=2010_10458,
-                     step4=a.step4, levels_per_pass=a.levels, uid=uid, stream=stream, device=local, ag_mode=a.ag_mode)
+                     step4=a.step4, levels_per_pass=a.levels, uid=uid, stream=stream, device=local, ag_mode=a.ag_mode,
+                     select=a.select)
     L, k = ctx.seg_len, ctx.k
     log("ctx up")
     # inputs: a fresh seeded N(0,1) gradient for every warm-up / timed / profiled step, generated on
@@ -401,7 +406,7 @@ def main():
                 "dtype": "f32", "data": "synthetic",
                 "config": {"workload": workload_name(a, P), "d": a.d, "rho": a.rho, "k": k, "n_iters": a.n_iters,
                            "P": P, "group_size": n, "step4": a.step4 if n > 1 else None, "dist": a.dist,
-                           "allgather": (a.ag_mode if n == 1 and P > 1 else None),
+                           "allgather": (a.ag_mode if n == 1 and P > 1 else None), "selector": a.select,
                            "levels_per_pass": a.levels or 4, "input_buffers": nbuf,
                            "inputs": "fresh seeded N(0,1) gradient per step (torch CUDA generator, pre-generated in "
                                      "HBM); residual carried from r=0 at step 0; timed steps W..W+K-1",

@@ -58,6 +58,11 @@ enum { TK_AG_PUSH = 0, TK_AG_NCCL = 1 };          /* flat sparse all-gather (A9)
                                                      PUSH = the compression writes its pairs into
                                                      every peer's buffer over NVLink (P <= 8);
                                                      NCCL = ncclAllGather after the compression */
+enum { TK_SELECT_MSTOPK = 0, TK_SELECT_EXACT = 1 }; /* selector:
+                                                     MSTOPK = Alg. 1 under Q1-Q27;
+                                                     EXACT = exact top-k of Eq. 2:
+                                                     the k largest |acc|, ties -> lower index (Q6);
+                                                     n_iters is then unused                     */
 enum { TK_RS_ORDERED = 0, TK_RS_NCCL = 1 };       /* HiTopKComm step 1 reduce-scatter (Q20):
                                                      ORDERED = ascending-row-rank fp32 sum read over
                                                      NVLink peer pointers inside the EF kernel
@@ -84,6 +89,7 @@ typedef struct tk_config {
   int32_t device;          /* CUDA device ordinal to use (-1 = current)                        */
   uint32_t rs_mode;        /* HiTopKComm step-1 mode (TK_RS_ORDERED or TK_RS_NCCL)             */
   uint32_t ag_mode;        /* flat all-gather mode (TK_AG_PUSH or TK_AG_NCCL)                  */
+  uint32_t select;         /* TK_SELECT_MSTOPK (default) or TK_SELECT_EXACT                    */
 } tk_config;
 
 /* Snapshot of the last compression's MSTopK control block (for parity checks). */

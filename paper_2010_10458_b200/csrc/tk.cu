@@ -39,7 +39,7 @@ struct tk_ctx {
   int lev_sched[NMAX];
   uint32_t units_per_warp = 1;        // ef phase: aligned power-of-two run of 512-element units per warp
   uint32_t* cta_cls = nullptr;        // [2][grid] per-CTA class counts
-  uint32_t* totals = nullptr;         // [npass][16] trial totals
+  uint32_t* totals = nullptr;         // [npass][HREP][256] pass totals / histograms
   uint32_t* bar = nullptr;            // grid barrier words [2] + flags [2]
   uint32_t* flags = nullptr;
   double* cta_sum = nullptr;          // K1 per-CTA partial sums / maxima
@@ -133,18 +133,23 @@ SearchParams search_params(const tk_ctx* c) {
   return sp;
 }
 
-const void* compress_kernel(bool ef, int np) {
+template <int SEL>
+const void* compress_kernel_sel(bool ef, int np) {
   switch ((ef ? 100 : 0) + np) {
-    case 100: return reinterpret_cast<const void*>(&k_compress<true, 0>);
-    case 102: return reinterpret_cast<const void*>(&k_compress<true, 2>);
-    case 104: return reinterpret_cast<const void*>(&k_compress<true, 4>);
-    case 108: return reinterpret_cast<const void*>(&k_compress<true, 8>);
-    case 0: return reinterpret_cast<const void*>(&k_compress<false, 0>);
-    case 2: return reinterpret_cast<const void*>(&k_compress<false, 2>);
-    case 4: return reinterpret_cast<const void*>(&k_compress<false, 4>);
-    case 8: return reinterpret_cast<const void*>(&k_compress<false, 8>);
+    case 100: return reinterpret_cast<const void*>(&k_compress<true, 0, SEL>);
+    case 102: return reinterpret_cast<const void*>(&k_compress<true, 2, SEL>);
+    case 104: return reinterpret_cast<const void*>(&k_compress<true, 4, SEL>);
+    case 108: return reinterpret_cast<const void*>(&k_compress<true, 8, SEL>);
+    case 0: return reinterpret_cast<const void*>(&k_compress<false, 0, SEL>);
+    case 2: return reinterpret_cast<const void*>(&k_compress<false, 2, SEL>);
+    case 4: return reinterpret_cast<const void*>(&k_compress<false, 4, SEL>);
+    case 8: return reinterpret_cast<const void*>(&k_compress<false, 8, SEL>);
   }
   return nullptr;
+}
+
+const void* compress_kernel(bool ef, int np, uint32_t sel) {
+  return sel == TK_SELECT_EXACT ? compress_kernel_sel<SEL_EXACT>(ef, np) : compress_kernel_sel<SEL_MSTOPK>(ef, np);
 }
 
 int peer_sources(const tk_ctx* c) { return (c->n > 1 && c->cfg.rs_mode == TK_RS_ORDERED) ? (int)c->n : 0; }
@@ -180,7 +185,7 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.lev0 = c->lev_sched[0];
   f.cap_levels = (int)c->levels;
   f.max_pass = (int)c->npass;
-  const void* kern = compress_kernel(ef, np);
+  const void* kern = compress_kernel(ef, np, c->cfg.select);
   if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
   void* args[] = {&f};
   TK_CUDA(c, cudaLaunchCooperativeKernel(kern, dim3(c->grid), dim3(THREADS), args, 0, c->stream));
@@ -220,7 +225,7 @@ tk_status plan_launches(tk_ctx* c) {
   TK_CUDA(c, cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, c->device));
   c->sms = (uint32_t)v;
   int occ = 0, o7 = 0;
-  const void* kern = compress_kernel(c->cfg.error_feedback != 0, peer_sources(c));
+  const void* kern = compress_kernel(c->cfg.error_feedback != 0, peer_sources(c), c->cfg.select);
   if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count");
   TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0));
   TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o7, k_decompress<PlainChunks>, THREADS, 64 * sizeof(uint32_t)));
@@ -238,7 +243,7 @@ tk_status plan_launches(tk_ctx* c) {
   TK_TRY(dev_alloc(c, &c->cta_sum, c->grid));
   TK_TRY(dev_alloc(c, &c->cta_max, c->grid));
   TK_TRY(dev_alloc(c, &c->cta_cls, 3 * (size_t)c->grid));
-  TK_TRY(dev_alloc(c, &c->totals, (size_t)HIST_BINS * c->npass));
+  TK_TRY(dev_alloc(c, &c->totals, (size_t)HIST_BINS * HREP * c->npass));
   TK_TRY(dev_alloc(c, &c->bar, 4));
   TK_CUDA(c, cudaMemset(c->bar, 0, 4 * sizeof(uint32_t)));
   c->flags = c->bar + 2;
@@ -355,7 +360,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if (k.n_iters < 1 || k.n_iters > (uint32_t)NMAX) return TK_ERR_INVALID_ARG;
   if (k.nranks < 1 || k.rank >= k.nranks) return TK_ERR_INVALID_ARG;
   if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 8 || k.rs_mode > 1 ||
-      k.ag_mode > 1)
+      k.ag_mode > 1 || k.select > 1)
     return TK_ERR_INVALID_ARG;
   const uint32_t n = k.group_size == 0 ? 1 : k.group_size;
   if (k.nranks % n != 0) return TK_ERR_CONFIG;
@@ -395,6 +400,9 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
     c->lev_sched[0] = (int)first;
     const uint32_t per = std::min<uint32_t>(2u, c->levels);
     c->npass = 1 + (k.n_iters - 1 + per - 1) / per;  // worst case: the first pass resolves one level
+    // exact selector: <= 2 compacting passes + <= 16 whole-vector passes (2 bits each over the
+    // 31-bit key space) + <= 4 histogram passes (8 bits each) + the final per-warp count
+    if (k.select == TK_SELECT_EXACT) c->npass = 24;
   }
   auto bail = [&](tk_status s) {
     free_all(c);
@@ -607,7 +615,8 @@ tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
   st->mean = h.abar;
   st->max_bits = h.umax_bits;
   st->n_trials = h.it;
-  for (uint32_t i = 0; i < h.it && i < (uint32_t)NMAX; ++i) {
+  // the exact selector keeps no trial log (n_trials = its narrowing passes)
+  for (uint32_t i = 0; c->cfg.select == TK_SELECT_MSTOPK && i < h.it && i < (uint32_t)NMAX; ++i) {
     st->ratio[i] = h.ratio_log[i];
     st->thres[i] = h.thres_log[i];
     st->key[i] = h.key_log[i];

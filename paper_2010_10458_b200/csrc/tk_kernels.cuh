@@ -22,6 +22,10 @@ constexpr int TMAX = 15;            // max candidates per count pass (4 bisectio
 constexpr int NMAX = 52;            // max MSTopK samplings (Q5)
 constexpr uint32_t INF_BITS = 0x7F800000u;
 constexpr uint32_t NO_INDEX = 0xFFFFFFFFu;
+// Global pass totals / histograms are replicated HREP times (copy = CTA index mod HREP) so the
+// CTAs' atomic adds spread over HREP addresses per bin; readers sum the copies.
+constexpr int HREP = 8;
+constexpr int TOT_STRIDE = 256;  // words per copy (= HIST_BINS)
 
 // Device-resident MSTopK control block (Alg. 1 l.4-6 state + the trial log).
 struct Ctrl {
@@ -57,6 +61,11 @@ struct Ctrl {
   uint32_t n_phase;
   uint32_t n_compacted;  // entries kept by the first count pass (all warps)
   uint32_t cand_tree;    // the candidates form a complete subtree (walked by index in replay)
+  // exact selector (TK_SELECT_EXACT): bracket [xlo, xhi) of the k-th largest key T with
+  // xcnt_lo = #{a >= xlo} >= k > xcnt_hi = #{a >= xhi}; prev_T = the previous call's T (0: none)
+  uint32_t xlo, xhi, xcnt_lo, xcnt_hi;
+  uint32_t prev_T, prev_dT;  // the previous call's T and how far T moved in that call
+  uint32_t xretry;       // a whole-vector compaction retry was spent
 };
 
 // Per-launch parameters of the MSTopK kernels.  The count and selection kernels share one
@@ -756,7 +765,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
     uint32_t tot = 0;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) tot += s_cnt[w][threadIdx.x];
-    atomicAdd(&totals[threadIdx.x], tot);
+    atomicAdd(&totals[(blockIdx.x & (HREP - 1)) * TOT_STRIDE + threadIdx.x], tot);
   }
   __syncthreads();
 }
@@ -816,7 +825,17 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
     uint32_t t = 0;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) t += s_h[w][b];
-    if (b > 0 && t) atomicAdd(ghist + b, t);  // bucket 0 (below every key) is never needed
+    if (b > 0 && t) atomicAdd(ghist + (blockIdx.x & (HREP - 1)) * TOT_STRIDE + b, t);  // bucket 0 is never needed
+  }
+  __syncthreads();
+}
+
+// the first nk pass totals (summed over the HREP copies) into shared memory
+__device__ __forceinline__ void load_totals(const uint32_t* tot_p, int nk, uint32_t* s_tot) {
+  if ((int)threadIdx.x < nk) {
+    uint32_t v = 0u;
+    for (int c = 0; c < HREP; ++c) v += __ldcg(tot_p + c * TOT_STRIDE + threadIdx.x);
+    s_tot[threadIdx.x] = v;
   }
   __syncthreads();
 }
@@ -827,7 +846,9 @@ __device__ __forceinline__ void hist_to_counts(const uint32_t* ghist, int lev, u
   const int NB = 1 << lev;
   // thread t owns bin NB-1-t (a reversed inclusive scan gives the suffix sums)
   const int b = NB - 1 - (int)threadIdx.x;
-  const uint32_t v = (b >= 1) ? __ldcg(ghist + b) : 0u;
+  uint32_t v = 0u;
+  if (b >= 1)
+    for (int c = 0; c < HREP; ++c) v += __ldcg(ghist + c * TOT_STRIDE + b);
   uint32_t total;
   const uint32_t excl = block_excl_scan(v, s_w, total);
   if (b >= 1) s_tot[b - 1] = excl + v;  // sum over bins b..NB-1 = nnz of candidate b-1
@@ -1072,10 +1093,37 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 template <int NK, int MODE>
 __device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass) {
-  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * pass, f.flags, pass);
+  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * HREP * pass, f.flags, pass);
 }
 
-template <bool EF, int NP>
+// ------------------------------------------------------------------------------------------
+// Exact selector (TK_SELECT_EXACT; Eq. 2, ties -> lower index, Q6): the k-th
+// largest magnitude key T is found by narrowing an integer bracket [xlo, xhi) over the 31-bit key
+// space with the same count / compaction / histogram passes: T = the largest key with
+// #{a >= key} >= k.  Then class 1 = {a > T} (all kept), class 2 = {a == T} with the window at 0
+// (the lowest indices), i.e. key1 = T + 1, key2 = T, rand = 0 in the MSTopK selection.
+enum { SEL_MSTOPK = 0, SEL_EXACT = 1 };
+
+// bracket update from counted keys (one thread)
+__device__ __forceinline__ void exact_update(Ctrl* c, const uint32_t* keys, const uint32_t* cnt, int nk, uint64_t k) {
+  for (int s = 0; s < nk; ++s) {
+    const uint32_t key = keys[s], n = cnt[s];
+    if ((uint64_t)n >= k) {
+      if (key > c->xlo) { c->xlo = key; c->xcnt_lo = n; }
+    } else if (key < c->xhi) {
+      c->xhi = key; c->xcnt_hi = n;
+    }
+  }
+}
+
+// nk keys splitting (xlo, xhi] evenly: xlo + ceil(j * w / (nk + 1)), j = 1..nk (ascending; with
+// w <= nk + 1 they cover every key of the bracket, so a pass always narrows it)
+__device__ __forceinline__ uint32_t exact_split(const Ctrl* c, uint32_t j, uint32_t parts) {
+  const uint64_t w = (uint64_t)c->xhi - c->xlo;
+  return c->xlo + (uint32_t)((j * w + parts - 1) / parts);
+}
+
+template <bool EF, int NP, int SEL>
 __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   __shared__ Ctrl sc;
   __shared__ uint32_t s_tot[HIST_BINS];
@@ -1092,16 +1140,147 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     sc.n_phase = (uint32_t)min(nph, 12);
   };
   stamp();
-  if (blockIdx.x == 0) {
-    for (int i = tid; i < HIST_BINS * f.max_pass; i += THREADS) f.totals[i] = 0u;
-    if (tid == 0) { f.flags[0] = 0u; f.flags[1] = 0u; }
-  }
+  for (int i = blockIdx.x * THREADS + tid; i < HIST_BINS * HREP * f.max_pass; i += gridDim.x * THREADS)
+    f.totals[i] = 0u;
+  if (blockIdx.x == 0 && tid == 0) { f.flags[0] = 0u; f.flags[1] = 0u; }
   // ---- A1-A2: error feedback, |acc| pairwise tree and max ----
   ef_phase<EF, NP>(f.g, f.pr, f.r, f.sp, f.units_per_warp, f.cta_sum, f.cta_max);
   grid_sync(f.bar);
   stamp();
   stats_root(f.cta_sum, f.cta_max, f.sp, &sc, f.step, f.lev0);
   stamp();
+  if constexpr (SEL == SEL_EXACT) {
+    const uint64_t k = f.sp.k;
+    // pass 0 (whole vector, compacting at key 0).  With a previous T: keys P - delta (the
+    // compaction key), P - 8 delta (a fallback lower bound) and P + delta, delta = twice the last
+    // move of T plus a margin; else u/4 (compaction key), u/2, u/8.  Any choice is exact: the
+    // compaction is used only if its key turns out to lie at or below T and no warp overflowed.
+    if (tid == 0) {
+      sc.xlo = 0u; sc.xcnt_lo = (uint32_t)f.sp.n;
+      sc.xhi = min(sc.umax_bits, 0x7FFFFFFFu) + 1u; sc.xcnt_hi = 0u;
+      sc.xretry = 0u;
+      const uint32_t P = sc.prev_T, u = sc.umax_bits;
+      auto sub = [](uint32_t a, uint32_t b) { return a > b ? a - b : 0u; };
+      if (P > 0u && P < sc.xhi) {
+        const uint32_t delta = min(1u << 22, 2u * min(sc.prev_dT, 1u << 22) + (1u << 10));
+        sc.cand_key[0] = sub(P, delta);
+        sc.cand_key[1] = sub(P, 8u * delta);
+        sc.cand_key[2] = min(P + delta, sc.xhi);
+      } else {
+        sc.cand_key[0] = sub(u, 2u << 23);
+        sc.cand_key[1] = sub(u, 1u << 23);
+        sc.cand_key[2] = sub(u, 3u << 23);
+      }
+      sc.cmp_key = sc.cand_key[0];
+      sc.ncand = 3u;
+      sc.it = 0u;
+    }
+    __syncthreads();
+    run_count<3, COUNT_FIRST>(f, &sc, 0);
+    grid_sync(f.bar);
+    stamp();
+    load_totals(f.totals, 3, s_tot);
+    __syncthreads();
+    if (tid == 0) {
+      exact_update(&sc, sc.cand_key, s_tot, 3, k);
+      sc.cap_ok = ((uint64_t)s_tot[0] >= k && __ldcg(f.flags) == 0u) ? 1u : 0u;
+      sc.it = 1u;
+    }
+    __syncthreads();
+    int p = 1;
+    __shared__ int s_mode;
+    while (sc.xhi > sc.xlo + 1u && p + 1 < f.max_pass) {
+      uint32_t* tot_p = f.totals + HIST_BINS * HREP * p;
+      if (tid == 0) {
+        if (sc.cap_ok) {
+          s_mode = 0;  // histogram of the compacted entries over 255 keys splitting the bracket
+        } else if (!sc.xretry && (uint64_t)sc.xcnt_lo * 8u <= f.sp.n) {
+          s_mode = 1;  // compact again at xlo (<= T, so exact unless a warp overflows)
+          sc.xretry = 1u;
+        } else {
+          s_mode = 2;  // whole-vector count of 3 keys
+        }
+      }
+      __syncthreads();
+      const int mode = s_mode;
+      if (mode == 0) {
+        if (tid < HIST_BINS - 1) sc.cand_key[tid] = exact_split(&sc, tid + 1, HIST_BINS);
+        __syncthreads();
+        hist_phase<HIST_LEV>(&sc, f.cp, tot_p, s_hist);
+      } else {
+        if (tid == 0) {
+          if (mode == 1) {
+            sc.cand_key[0] = sc.xlo;
+            sc.cand_key[1] = exact_split(&sc, 1, 3);
+            sc.cand_key[2] = exact_split(&sc, 2, 3);
+            sc.cmp_key = sc.xlo;
+          } else {
+            for (int j = 0; j < 3; ++j) sc.cand_key[j] = exact_split(&sc, j + 1, 4);
+          }
+        }
+        __syncthreads();
+        if (mode == 1)
+          count_phase<3, COUNT_FIRST>(f.acc, &sc, f.sp, f.wcnt, f.cp, tot_p, f.flags + 1, p);
+        else
+          run_count<3, COUNT_FULL>(f, &sc, p);
+      }
+      grid_sync(f.bar);
+      stamp();
+      if (mode == 0) {
+        hist_to_counts(tot_p, HIST_LEV, s_tot);
+      } else {
+        load_totals(tot_p, 3, s_tot);
+      }
+      if (tid == 0) {
+        if (mode == 0) {
+          // counts are non-increasing in the key: binary search for the last key with >= k
+          int lo = -1, hi = HIST_BINS - 1;  // s_tot[lo] >= k (lo = -1: none), s_tot[hi] < k (hi = 255: none)
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if ((uint64_t)s_tot[mid] >= k) lo = mid; else hi = mid;
+          }
+          if (lo >= 0) { sc.xlo = sc.cand_key[lo]; sc.xcnt_lo = s_tot[lo]; }
+          if (hi < HIST_BINS - 1) { sc.xhi = sc.cand_key[hi]; sc.xcnt_hi = s_tot[hi]; }
+        } else {
+          exact_update(&sc, sc.cand_key, s_tot, 3, k);
+          if (mode == 1) sc.cap_ok = (__ldcg(f.flags + 1) == 0u) ? 1u : 0u;
+        }
+        sc.it += 1u;
+      }
+      __syncthreads();
+      ++p;
+    }
+    // T = xlo: #{a > T} = xcnt_hi, #{a >= T} = xcnt_lo
+    if (!sc.cap_ok) {
+      // per-warp counts of a > T and a >= T for the selection's prefix sums (whole vector)
+      if (tid == 0) {
+        sc.cand_key[0] = sc.xlo + 1u;
+        sc.cand_key[1] = sc.xlo;
+      }
+      __syncthreads();
+      run_count<2, COUNT_FULL>(f, &sc, p);
+      grid_sync(f.bar);
+      stamp();
+    }
+    if (tid == 0) {
+      const uint32_t T = sc.xlo;
+      sc.k1 = sc.xcnt_hi;
+      sc.k2 = sc.xcnt_lo;
+      sc.key1 = T + 1u;
+      sc.key2 = T;
+      sc.thres1 = (double)__uint_as_float(T + 1u);
+      sc.thres2 = (double)__uint_as_float(T);
+      sc.prov1 = sc.cap_ok ? 0 : p * TMAX + 0;
+      sc.prov2 = sc.cap_ok ? 0 : p * TMAX + 1;
+      sc.need = (uint32_t)(k - sc.k1);
+      sc.len2 = (uint64_t)sc.k2 - sc.k1;
+      sc.rand = 0u;
+      const uint32_t P = sc.prev_T;
+      sc.prev_dT = (P > 0u) ? (T > P ? T - P : P - T) : (1u << 21);
+      sc.prev_T = T;
+    }
+    __syncthreads();
+  } else {
   // ---- A3-A5: count passes.  The first resolves lev0 levels on the whole vector and compacts;
   // when the compacted entries are exact for the rest, each further pass resolves up to HIST_LEV
   // levels on them at once (histogram pass), else up to 2 levels per pass on the whole vector.
@@ -1112,7 +1291,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   for (int p = 0; done < N; ++p) {
     int lev;
     bool hist = false;
-    uint32_t* tot_p = f.totals + HIST_BINS * p;
+    uint32_t* tot_p = f.totals + HIST_BINS * HREP * p;
     if (p == 0) {
       lev = f.lev0;  // keys along the predicted path
       if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, 0);
@@ -1140,8 +1319,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     if (hist) {
       hist_to_counts(tot_p, lev, s_tot);
     } else {
-      if (tid < 16) s_tot[tid] = __ldcg(tot_p + tid);
-      __syncthreads();
+      load_totals(tot_p, 16, s_tot);
     }
     if (tid == 0) {
       const double cmp_ratio = sc.cmp_ratio;
@@ -1161,6 +1339,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       __syncthreads();
     }
   }
+  }  // SEL_MSTOPK
   stamp();
   // ---- A7 prefix: class-1 / class-2 counts of each warp slab, then of the CTAs before it ----
   const uint32_t gw = blockIdx.x * WARPS + warp;

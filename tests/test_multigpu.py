@@ -82,3 +82,9 @@ def test_hitopk_zero_copy_input(tmp_path):
 def test_hitopk_c4_full_size(P, n, tmp_path):
     """BASELINE config 4: d = 25.6M HiTopKComm (2x4, 4x2 on 8 GPUs; 2x2 on 4)."""
     _run(P, tmp_path, dim=25_600_000, rho=0.001, group_size=n, steps=2)
+
+
+@pytest.mark.parametrize("P,n", [(2, 1), (4, 1), (4, 2)])
+def test_exact_selector_multi_gpu(P, n, tmp_path):
+    """the exact top-k selector (Eq. 2) on the flat push path and HiTopKComm"""
+    _run(P, tmp_path, dim=8 * 131_076, rho=0.001, group_size=n, select="exact", steps=3)

@@ -6,8 +6,9 @@ import torch
 import paper_2010_10458_b200 as tk
 
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 25_600_000
+select = sys.argv[2] if len(sys.argv) > 2 else "mstopk"
 steps = 60
-ctx = tk.Context(d, rho=0.001, n_iters=10, seed=1)
+ctx = tk.Context(d, rho=0.001, n_iters=10, seed=1, select=select)
 gen = torch.Generator(device="cuda")
 gen.manual_seed(5)
 gs = [torch.randn(d, generator=gen, device="cuda") for _ in range(8)]
@@ -21,6 +22,8 @@ for s in range(steps):
         acc = st.phase_us if acc is None else [a + b for a, b in zip(acc, st.phase_us)]
 n = steps - 20
 names = ["ef", "root"] + [f"pass{i}" for i in range(len(acc) - 5)] + ["replay", "prefix", "select"]
-print("phases (us):", {names[i] if i < len(names) else i: round(v / n, 1) for i, v in enumerate(acc)},
+if select == "exact":
+    names = ["ef", "root"] + [f"pass{i}" for i in range(len(acc) - 4)] + ["prefix", "select"]
+print(select, "phases (us):", {names[i] if i < len(names) else i: round(v / n, 1) for i, v in enumerate(acc)},
       "total", round(sum(acc) / n, 1), "compacted", st.compacted, "n_compacted", st.n_compacted,
       "frac", round(st.n_compacted / d, 4))
