@@ -109,13 +109,18 @@ typedef struct tk_stats {
   uint64_t rand_start;     /* rand (l.27)                                                      */
   uint64_t step;           /* step counter used for this compression's RNG draw               */
   uint32_t nonfinite;      /* 1 if a NaN/Inf was seen (sticky)                                 */
-  uint32_t compacted;      /* 1 if passes 2.. and the selection ran on the entries compacted by
-                              the first count pass (an exact shortcut)          */
-  uint32_t n_compacted;    /* entries the first count pass kept (when compacted)                */
+  uint32_t compacted;      /* 1 if later passes and the selection ran on compacted entries
+                              (an exact shortcut)                               */
+  uint32_t n_compacted;    /* entries kept (when compacted)                                     */
   uint32_t n_phases;       /* phase boundaries recorded in phase_ns                             */
   uint64_t phase_ns[12];   /* device %globaltimer (ns) at k_compress's phase boundaries (CTA 0,
                               after each grid barrier): start, stats, each count pass, prefix,
                               end of selection                                                 */
+  uint32_t ef_compacted;   /* 1 if the entries were compacted inside the EF pass at the key the
+                              previous call predicted (no whole-vector count pass ran)         */
+  uint64_t nnz_lower_bound;/* bit i set: trial i's threshold lay below that compaction key, so
+                              nnz[i] is a lower bound of the count, and > k (the decision and
+                              every result are exact)                           */
 } tk_stats;
 
 /* k = max(1, floor(rho * d)) in fp64 (Q13).  Host-only, pure.  0 on invalid input. */

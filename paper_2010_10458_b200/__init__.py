@@ -53,7 +53,8 @@ class _Stats(ctypes.Structure):
                 ("len2", ctypes.c_uint64), ("rand_start", ctypes.c_uint64), ("step", ctypes.c_uint64),
                 ("nonfinite", ctypes.c_uint32), ("compacted", ctypes.c_uint32), ("n_compacted", ctypes.c_uint32),
                 ("n_phases", ctypes.c_uint32),
-                ("phase_ns", ctypes.c_uint64 * 12)]
+                ("phase_ns", ctypes.c_uint64 * 12), ("ef_compacted", ctypes.c_uint32),
+                ("nnz_lower_bound", ctypes.c_uint64)]
 
 
 # Every symbol include/tk.h declares (checked by tests/test_abi.py).
@@ -173,6 +174,8 @@ class Stats:
     compacted: bool
     n_compacted: int
     phase_us: list  # k_compress phase durations (device globaltimer, CTA 0)
+    ef_compacted: bool  # the entries came from the EF pass (predicted key), no whole-vector count pass
+    nnz_lower_bound: int  # bit i: trials[i]'s nnz is a lower bound (> k) - its threshold lay below that key
 
 
 class _DeviceView:
@@ -288,7 +291,8 @@ class Context:
                      thres2=s.thres2, thres1_set=bool(s.thres1_set), thres2_set=bool(s.thres2_set), key1=s.key1,
                      key2=s.key2, len2=s.len2, rand=s.rand_start, step=s.step, nonfinite=bool(s.nonfinite),
                      compacted=bool(s.compacted), n_compacted=int(s.n_compacted),
-                     phase_us=[(s.phase_ns[i + 1] - s.phase_ns[i]) / 1e3 for i in range(max(0, s.n_phases - 1))])
+                     phase_us=[(s.phase_ns[i + 1] - s.phase_ns[i]) / 1e3 for i in range(max(0, s.n_phases - 1))],
+                     ef_compacted=bool(s.ef_compacted), nnz_lower_bound=int(s.nnz_lower_bound))
 
     def input_buffer(self):
         """HiTopKComm ordered mode: a torch view of libtk's peer-visible gradient buffer (write the

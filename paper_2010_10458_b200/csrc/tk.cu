@@ -36,6 +36,7 @@ struct tk_ctx {
   uint64_t S = 0;                     // slab length
   uint32_t occ_dec = 1;               // resident decompression CTAs per SM
   uint32_t levels = 4, npass = 0;
+  uint32_t ef_compact = 1;            // compaction in the ef phase (TK_EF_COMPACT=0 disables; bits unchanged)
   int lev_sched[NMAX];
   uint32_t units_per_warp = 1;        // ef phase: aligned power-of-two run of 512-element units per warp
   uint32_t* cta_cls = nullptr;        // [2][grid] per-CTA class counts
@@ -185,6 +186,7 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.lev0 = c->lev_sched[0];
   f.cap_levels = (int)c->levels;
   f.max_pass = (int)c->npass;
+  f.ef_compact = c->ef_compact;
   const void* kern = compress_kernel(ef, np, c->cfg.select);
   if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
   void* args[] = {&f};
@@ -242,10 +244,10 @@ tk_status plan_launches(tk_ctx* c) {
   c->S = upw * ROUND;  // count / select slabs = the ef phase's warp runs (acc is re-read from L2)
   TK_TRY(dev_alloc(c, &c->cta_sum, c->grid));
   TK_TRY(dev_alloc(c, &c->cta_max, c->grid));
-  TK_TRY(dev_alloc(c, &c->cta_cls, 3 * (size_t)c->grid));
+  TK_TRY(dev_alloc(c, &c->cta_cls, 4 * (size_t)c->grid));
   TK_TRY(dev_alloc(c, &c->totals, (size_t)HIST_BINS * HREP * c->npass));
-  TK_TRY(dev_alloc(c, &c->bar, 4));
-  TK_CUDA(c, cudaMemset(c->bar, 0, 4 * sizeof(uint32_t)));
+  TK_TRY(dev_alloc(c, &c->bar, 8));
+  TK_CUDA(c, cudaMemset(c->bar, 0, 8 * sizeof(uint32_t)));
   c->flags = c->bar + 2;
   // compacted entries: capacity S/4 per warp slab (the whole-vector path covers an overflow)
   c->cp.C = (uint32_t)std::max<uint64_t>(4, (c->S / 4 + 3) / 4 * 4);
@@ -403,6 +405,8 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
     // exact selector: <= 2 compacting passes + <= 16 whole-vector passes (2 bits each over the
     // 31-bit key space) + <= 4 histogram passes (8 bits each) + the final per-warp count
     if (k.select == TK_SELECT_EXACT) c->npass = 24;
+    else c->npass += k.n_iters;  // an ef-phase search (>= 1 level per pass) may precede a restart
+    if (const char* e = getenv("TK_EF_COMPACT")) c->ef_compact = atoi(e) != 0 ? 1u : 0u;
   }
   auto bail = [&](tk_status s) {
     free_all(c);
@@ -638,6 +642,8 @@ tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
   st->nonfinite = c->nonfinite_sticky;
   st->compacted = h.cap_ok;
   st->n_compacted = h.n_compacted;
+  st->ef_compacted = h.ef_used;
+  st->nnz_lower_bound = h.nnz_lb;
   st->n_phases = std::min<uint32_t>(12, h.n_phase);
   for (int i = 0; i < 12; ++i) st->phase_ns[i] = h.phase_ns[i];
   if (c->nonfinite_sticky) return fail(c, TK_ERR_NONFINITE, "non-finite value in acc (precondition, Q24)");

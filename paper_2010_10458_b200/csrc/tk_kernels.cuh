@@ -66,7 +66,13 @@ struct Ctrl {
   uint32_t xlo, xhi, xcnt_lo, xcnt_hi;
   uint32_t prev_T, prev_dT;  // the previous call's T and how far T moved in that call
   uint32_t xretry;       // a whole-vector compaction retry was spent
+  uint32_t cmp_bottom;   // the entries sit at the bottom of the warp regions (ef-phase compaction)
+  uint32_t ef_key;       // compaction key of the NEXT call's ef phase (0: none), set at the end of a call
+  uint32_t ef_used;      // this call's selection ran on the ef-phase entries
+  uint32_t prev_key2;    // MSTopK: the previous call's key2
+  uint64_t nnz_lb;       // trials whose logged nnz is a lower bound (> k): below the ef-phase key
 };
+
 
 // Per-launch parameters of the MSTopK kernels.  The count and selection kernels share one
 // partition of [0, n) into W contiguous warp slabs of S elements (S a multiple of ROUND).
@@ -91,6 +97,12 @@ struct Compact {
   uint32_t* cnt;
   uint32_t C;  // capacity per warp (multiple of 4)
 };
+
+// first entry of warp gw's compacted entries (ne of them): top of the region for the count
+// pass's compaction, bottom for the ef phase's
+__device__ __forceinline__ uint32_t entry_off(const Compact& cp, uint32_t ne, uint32_t bottom) {
+  return bottom ? 0u : cp.C - ne;
+}
 
 // TK_AG_PUSH (fused all-gather): slot[q] = this rank's chunk of peer q's gathered buffer (q == me:
 // the local one).  A pair travels as one 16-byte packet of two 8-byte words {idx, tag} and
@@ -131,9 +143,16 @@ struct TaggedChunks {  // [nchunks][k] tagged packets, written by the peers duri
   __device__ __forceinline__ void get(uint32_t p, uint32_t j, uint32_t& i, float& v) const {
     const ulonglong2* a = g + (size_t)p * k + j;
     ulonglong2 x = ld_ll(a);
-    while ((uint32_t)(x.x >> 32) != tag || (uint32_t)(x.y >> 32) != tag) {
-      __nanosleep(32);
-      x = ld_ll(a);
+    if ((uint32_t)(x.x >> 32) != tag || (uint32_t)(x.y >> 32) != tag) {
+      uint64_t t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      do {
+        __nanosleep(32);
+        x = ld_ll(a);
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 5000000000ull) __trap();  // a peer never delivered (5 s): fail loudly, never hang
+      } while ((uint32_t)(x.x >> 32) != tag || (uint32_t)(x.y >> 32) != tag);
     }
     i = (uint32_t)x.x;
     v = __uint_as_float((uint32_t)x.y);
@@ -348,6 +367,40 @@ __device__ __forceinline__ uint32_t quad_max_bits(float4 v) {
   return max(max(a, b), max(c, d));
 }
 
+// Candidates of the whole-vector first count pass: the nodes along the path toward the bracket
+// the previous compression ended in; the compaction key is the highest of them at or below that
+// bracket (any choice is exact; a good one keeps few elements).  One thread.
+__device__ void first_pass_candidates(Ctrl* sc, int first_levels) {
+  make_candidates_path(sc, first_levels, sc->prev_lo);
+  int ms = 0;
+  for (int q = 1; q < (int)sc->ncand; ++q)
+    if (sc->cand_ratio[q] <= sc->prev_lo && sc->cand_ratio[q] > sc->cand_ratio[ms]) ms = q;
+  if (sc->cand_ratio[ms] > sc->prev_lo) {  // no candidate below the prediction: take the lowest
+    for (int q = 1; q < (int)sc->ncand; ++q)
+      if (sc->cand_ratio[q] < sc->cand_ratio[ms]) ms = q;
+  }
+  // the compaction key becomes candidate 0, so the first pass's compaction test is the same
+  // compare as its count of that key (the replay finds candidates by ratio, order-free)
+  if (ms != 0) {
+    const double r0 = sc->cand_ratio[0], t0 = sc->cand_t[0];
+    const uint32_t k0 = sc->cand_key[0];
+    sc->cand_ratio[0] = sc->cand_ratio[ms]; sc->cand_t[0] = sc->cand_t[ms]; sc->cand_key[0] = sc->cand_key[ms];
+    sc->cand_ratio[ms] = r0; sc->cand_t[ms] = t0; sc->cand_key[ms] = k0;
+  }
+  sc->cmp_key = sc->cand_key[0];
+  sc->cmp_ratio = sc->cand_ratio[0];
+}
+
+// Alg. 1 l.4-6: the search state before the first trial
+__device__ __forceinline__ void search_reset(Ctrl* c, uint64_t n) {
+  c->lo = 0.0; c->hi = 1.0;                             // l.4
+  c->k1 = 0u; c->k2 = (uint32_t)n;                      // l.5
+  c->thres1 = 0.0; c->thres2 = 0.0;                     // l.6
+  c->key1 = INF_BITS; c->key2 = 0u;                     // Q8 / Q9 sentinels
+  c->prov1 = -1; c->prov2 = -1;
+  c->it = 0u;
+}
+
 __device__ void stats_finalize(Ctrl* c, const SearchParams& sp, double S, uint32_t m, uint64_t step,
                                int first_levels) {
   c->prev_lo = c->lo;
@@ -355,12 +408,7 @@ __device__ void stats_finalize(Ctrl* c, const SearchParams& sp, double S, uint32
   c->umax_bits = m;                                     // Alg. 1 l.3
   c->U = (double)__uint_as_float(m);
   c->nonfinite = (m >= INF_BITS) ? 1u : 0u;
-  c->lo = 0.0; c->hi = 1.0;                             // l.4
-  c->k1 = 0u; c->k2 = (uint32_t)sp.n;                   // l.5
-  c->thres1 = 0.0; c->thres2 = 0.0;                     // l.6
-  c->key1 = INF_BITS; c->key2 = 0u;                     // Q8 / Q9 sentinels
-  c->prov1 = -1; c->prov2 = -1;
-  c->it = 0u;
+  search_reset(c, sp.n);
   c->step = step;
   (void)first_levels;
 }
@@ -415,15 +463,28 @@ __device__ __forceinline__ void ef_load(const float* g, const Peers& pr, const f
   }
 }
 
+// Optional compaction (ckey > 0, a key predicted by the previous call): every element with
+// bits(|acc|) >= ckey is appended, in index order, to the warp's entries at the BOTTOM of its
+// region ([0, cnt)); the warp's units are exactly its count-pass slab.  Per-CTA entry totals go
+// to cta_ent, a warp holding more than the capacity sets *overflow.
 template <bool EF, int NP>
 __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peers& pr, float* __restrict__ r,
                                          const SearchParams& sp, uint32_t units_per_warp,
-                                         double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max) {
+                                         double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max,
+                                         uint32_t ckey, const Compact cp, uint32_t* overflow,
+                                         uint32_t* __restrict__ cta_ent) {
   __shared__ double s_ws[WARPS];
   __shared__ uint32_t s_wm[WARPS];
+  __shared__ uint32_t s_we[WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t n = sp.n;
-  const uint64_t u0 = ((uint64_t)blockIdx.x * WARPS + warp) * units_per_warp;
+  const uint32_t gw = blockIdx.x * WARPS + warp;
+  const uint64_t u0 = (uint64_t)gw * units_per_warp;
+  const bool cmp_on = ckey > 0u;
+  const int32_t ckm1 = (int32_t)ckey - 1;
+  uint32_t ncomp = 0;
+  uint32_t* oi = cp.idx + (size_t)gw * cp.C;
+  uint32_t* ob = cp.bits + (size_t)gw * cp.C;
   double stk[24];
   uint32_t mx = 0;
   // NP == 0: the next unit's loads are issued before this unit is reduced (one unit in flight
@@ -480,6 +541,49 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
         if (nfull) ef_load<EF, NP>(g, pr, r, base + ROUND, ng, nr);
       }
     }
+    if (cmp_on) {
+      // element (ch, lane, e) has index u*512 + ch*128 + 4*lane + e: chunk-major, then lane, then
+      // e is index order; one packed scan (a byte per chunk) places every hit of the unit
+      uint32_t m = 0;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t w4[4] = {__float_as_uint(acc[ch].x), __float_as_uint(acc[ch].y), __float_as_uint(acc[ch].z),
+                                __float_as_uint(acc[ch].w)};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m |= ((uint32_t)(ckm1 - (int32_t)(w4[e] & 0x7FFFFFFFu)) >> 31) << (4 * ch + e);
+      }
+      if (__any_sync(0xffffffffu, m != 0u)) {
+        const uint32_t packed = __popc(m & 0xFu) | (__popc((m >> 4) & 0xFu) << 8) | (__popc((m >> 8) & 0xFu) << 16) |
+                                (__popc(m >> 12) << 24);
+        uint32_t incl = packed;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += o;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t excl = incl - packed;
+        uint32_t cb = ncomp;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pos = cb + ((excl >> (8 * ch)) & 0xFFu);
+          const uint32_t w4[4] = {__float_as_uint(acc[ch].x), __float_as_uint(acc[ch].y), __float_as_uint(acc[ch].z),
+                                  __float_as_uint(acc[ch].w)};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (m & (1u << (4 * ch + e))) {
+              if (pos < cp.C) {
+                oi[pos] = (uint32_t)(u * ROUND + ch * 128 + 4 * lane + e);
+                ob[pos] = w4[e];
+              }
+              ++pos;
+            }
+          }
+          cb += (tot >> (8 * ch)) & 0xFFu;
+        }
+        ncomp = cb;
+      }
+    }
     double cs[4];
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) {
@@ -500,9 +604,18 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   if (lane == 0) {
     s_ws[warp] = stk[top];
     s_wm[warp] = mx;
+    s_we[warp] = ncomp;
+    if (cmp_on) {
+      cp.cnt[gw] = ncomp;
+      if (ncomp > cp.C) atomicOr(overflow, 1u);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    uint32_t te = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) te += s_we[w];
+    cta_ent[blockIdx.x] = te;
     cta_sum[blockIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(s_ws[0], s_ws[1]), __dadd_rn(s_ws[2], s_ws[3])),
                                     __dadd_rn(__dadd_rn(s_ws[4], s_ws[5]), __dadd_rn(s_ws[6], s_ws[7])));
     uint32_t m = s_wm[0];
@@ -563,28 +676,7 @@ __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* _
     stats_finalize(sc, sp, s_v[0], m, step, first_levels);
   }
   __syncthreads();
-  if (tid == 0) {
-    make_candidates_path(sc, first_levels, sc->prev_lo);
-    // compaction key of the first count pass: the highest of its candidates at or below the
-    // bracket the previous compression ended in (any choice is exact; a good one keeps few elements)
-    int ms = 0;
-    for (int q = 1; q < (int)sc->ncand; ++q)
-      if (sc->cand_ratio[q] <= sc->prev_lo && sc->cand_ratio[q] > sc->cand_ratio[ms]) ms = q;
-    if (sc->cand_ratio[ms] > sc->prev_lo) {  // no candidate below the prediction: take the lowest
-      for (int q = 1; q < (int)sc->ncand; ++q)
-        if (sc->cand_ratio[q] < sc->cand_ratio[ms]) ms = q;
-    }
-    // the compaction key becomes candidate 0, so the first pass's compaction test is the same
-    // compare as its count of that key (the replay finds candidates by ratio, order-free)
-    if (ms != 0) {
-      const double r0 = sc->cand_ratio[0], t0 = sc->cand_t[0];
-      const uint32_t k0 = sc->cand_key[0];
-      sc->cand_ratio[0] = sc->cand_ratio[ms]; sc->cand_t[0] = sc->cand_t[ms]; sc->cand_key[0] = sc->cand_key[ms];
-      sc->cand_ratio[ms] = r0; sc->cand_t[ms] = t0; sc->cand_key[ms] = k0;
-    }
-    sc->cmp_key = sc->cand_key[0];
-    sc->cmp_ratio = sc->cand_ratio[0];
-  }
+  if (tid == 0) first_pass_candidates(sc, first_levels);
   __syncthreads();
 }
 
@@ -626,7 +718,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
   };
   if (MODE == COUNT_CAP) {
     const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-    const uint32_t* eb = cp.bits + (size_t)gw * cp.C + (cp.C - ne);  // entries sit at the region's top
+    const uint32_t* eb = cp.bits + (size_t)gw * cp.C + entry_off(cp, ne, sc->cmp_bottom);
     // this warp's entry loads in flight together (4 x 128 entries per iteration)
     for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
       uint4 q[4];
@@ -794,7 +886,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
   __syncthreads();
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-  const uint32_t* eb = cp.bits + (size_t)gw * cp.C + (cp.C - ne);  // entries sit at the region's top
+  const uint32_t* eb = cp.bits + (size_t)gw * cp.C + entry_off(cp, ne, sc->cmp_bottom);
   auto add = [&](uint32_t bits) {
     const int32_t a = (int32_t)(bits & 0x7FFFFFFFu);
     uint32_t b = 0;
@@ -882,8 +974,9 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
     // ---- compacted entries of this warp (ascending index order): 128 per iteration, lane l
     // holds entries 4l..4l+3 of the group, so (lane, e) order is index order ----
     const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-    const uint32_t* ei = cp.idx + (size_t)gw * cp.C + (cp.C - ne);  // entries sit at the region's top
-    const uint32_t* eb = cp.bits + (size_t)gw * cp.C + (cp.C - ne);
+    const uint32_t off = entry_off(cp, ne, c->cmp_bottom);
+    const uint32_t* ei = cp.idx + (size_t)gw * cp.C + off;
+    const uint32_t* eb = cp.bits + (size_t)gw * cp.C + off;
     for (uint32_t j0 = 0; j0 < ne; j0 += 128) {
       const uint32_t j = j0 + 4 * lane;
       uint32_t bb[4] = {0u, 0u, 0u, 0u}, ii[4] = {0u, 0u, 0u, 0u};
@@ -1063,6 +1156,7 @@ struct Fused {
   int lev0;                  // levels of the first (whole-vector) pass: min(2, N, cap_levels)
   int cap_levels;            // max levels per later pass on compacted entries (whole-vector: <= 2)
   int max_pass;              // passes for which totals / wcnt are allocated
+  uint32_t ef_compact;       // 1: compact in the ef phase at the key the previous call predicted
 };
 
 // Grid-wide barrier (the launch is cooperative: every CTA is resident).  Arrivals are counted
@@ -1142,52 +1236,82 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   stamp();
   for (int i = blockIdx.x * THREADS + tid; i < HIST_BINS * HREP * f.max_pass; i += gridDim.x * THREADS)
     f.totals[i] = 0u;
-  if (blockIdx.x == 0 && tid == 0) { f.flags[0] = 0u; f.flags[1] = 0u; }
-  // ---- A1-A2: error feedback, |acc| pairwise tree and max ----
-  ef_phase<EF, NP>(f.g, f.pr, f.r, f.sp, f.units_per_warp, f.cta_sum, f.cta_max);
+  if (blockIdx.x == 0 && tid == 0) { f.flags[0] = 0u; f.flags[1] = 0u; f.flags[2] = 0u; }
+  // ---- A1-A2: error feedback, |acc| pairwise tree and max; compaction at the key the previous
+  // call predicted (its entries replace the whole-vector first count pass when they are exact) ----
+  const uint32_t efk = f.ef_compact ? sc.ef_key : 0u;
+  uint32_t* cta_ent = f.cta_cls + 3 * gridDim.x;
+  ef_phase<EF, NP>(f.g, f.pr, f.r, f.sp, f.units_per_warp, f.cta_sum, f.cta_max, efk, f.cp, f.flags + 2, cta_ent);
   grid_sync(f.bar);
   stamp();
   stats_root(f.cta_sum, f.cta_max, f.sp, &sc, f.step, f.lev0);
   stamp();
+  const bool ef_ok = efk > 0u && __ldcg(f.flags + 2) == 0u;  // entries = {a >= efk}, none dropped
+  if (tid == 0) { sc.cmp_bottom = 0u; sc.cap_ok = 0u; sc.ef_used = 0u; sc.nnz_lb = 0ull; }
+  __syncthreads();
   if constexpr (SEL == SEL_EXACT) {
     const uint64_t k = f.sp.k;
-    // pass 0 (whole vector, compacting at key 0).  With a previous T: keys P - delta (the
-    // compaction key), P - 8 delta (a fallback lower bound) and P + delta, delta = twice the last
-    // move of T plus a margin; else u/4 (compaction key), u/2, u/8.  Any choice is exact: the
-    // compaction is used only if its key turns out to lie at or below T and no warp overflowed.
+    __shared__ uint32_t s_e;
+    if (ef_ok) {  // E = #{a >= efk}
+      uint32_t e = 0;
+      for (uint32_t b = tid; b < gridDim.x; b += THREADS) e += __ldcg(cta_ent + b);
+      e = __reduce_add_sync(0xffffffffu, e);
+      if (lane == 0) s_w[0][warp] = e;
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < WARPS; ++w) t += s_w[0][w];
+        s_e = t;
+      }
+      __syncthreads();
+    }
+    int p = 0;
     if (tid == 0) {
       sc.xlo = 0u; sc.xcnt_lo = (uint32_t)f.sp.n;
       sc.xhi = min(sc.umax_bits, 0x7FFFFFFFu) + 1u; sc.xcnt_hi = 0u;
       sc.xretry = 0u;
-      const uint32_t P = sc.prev_T, u = sc.umax_bits;
-      auto sub = [](uint32_t a, uint32_t b) { return a > b ? a - b : 0u; };
-      if (P > 0u && P < sc.xhi) {
-        const uint32_t delta = min(1u << 22, 2u * min(sc.prev_dT, 1u << 22) + (1u << 10));
-        sc.cand_key[0] = sub(P, delta);
-        sc.cand_key[1] = sub(P, 8u * delta);
-        sc.cand_key[2] = min(P + delta, sc.xhi);
-      } else {
-        sc.cand_key[0] = sub(u, 2u << 23);
-        sc.cand_key[1] = sub(u, 1u << 23);
-        sc.cand_key[2] = sub(u, 3u << 23);
-      }
-      sc.cmp_key = sc.cand_key[0];
-      sc.ncand = 3u;
       sc.it = 0u;
+      if (ef_ok && (uint64_t)s_e >= k && efk < sc.xhi) {
+        // T >= efk: the ef-phase entries hold every element the narrowing and the selection need
+        sc.xlo = efk; sc.xcnt_lo = s_e;
+        sc.cap_ok = 1u; sc.cmp_bottom = 1u; sc.ef_used = 1u;
+      }
     }
     __syncthreads();
-    run_count<3, COUNT_FIRST>(f, &sc, 0);
-    grid_sync(f.bar);
-    stamp();
-    load_totals(f.totals, 3, s_tot);
-    __syncthreads();
-    if (tid == 0) {
-      exact_update(&sc, sc.cand_key, s_tot, 3, k);
-      sc.cap_ok = ((uint64_t)s_tot[0] >= k && __ldcg(f.flags) == 0u) ? 1u : 0u;
-      sc.it = 1u;
+    if (!sc.ef_used) {
+      // pass 0 (whole vector, compacting at key 0).  With a previous T: keys P - delta (the
+      // compaction key), P - 8 delta (a fallback lower bound) and P + delta, delta = twice the last
+      // move of T plus a margin; else u/4 (compaction key), u/2, u/8.  Any choice is exact: the
+      // compaction is used only if its key turns out to lie at or below T and no warp overflowed.
+      if (tid == 0) {
+        const uint32_t P = sc.prev_T, u = sc.umax_bits;
+        auto sub = [](uint32_t a, uint32_t b) { return a > b ? a - b : 0u; };
+        if (P > 0u && P < sc.xhi) {
+          const uint32_t delta = min(1u << 22, 2u * min(sc.prev_dT, 1u << 22) + (1u << 10));
+          sc.cand_key[0] = sub(P, delta);
+          sc.cand_key[1] = sub(P, 8u * delta);
+          sc.cand_key[2] = min(P + delta, sc.xhi);
+        } else {
+          sc.cand_key[0] = sub(u, 2u << 23);
+          sc.cand_key[1] = sub(u, 1u << 23);
+          sc.cand_key[2] = sub(u, 3u << 23);
+        }
+        sc.cmp_key = sc.cand_key[0];
+        sc.ncand = 3u;
+      }
+      __syncthreads();
+      run_count<3, COUNT_FIRST>(f, &sc, 0);
+      grid_sync(f.bar);
+      stamp();
+      load_totals(f.totals, 3, s_tot);
+      if (tid == 0) {
+        exact_update(&sc, sc.cand_key, s_tot, 3, k);
+        sc.cap_ok = ((uint64_t)s_tot[0] >= k && __ldcg(f.flags) == 0u) ? 1u : 0u;
+        sc.it = 1u;
+      }
+      __syncthreads();
+      p = 1;
     }
-    __syncthreads();
-    int p = 1;
     __shared__ int s_mode;
     while (sc.xhi > sc.xlo + 1u && p + 1 < f.max_pass) {
       uint32_t* tot_p = f.totals + HIST_BINS * HREP * p;
@@ -1226,11 +1350,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       }
       grid_sync(f.bar);
       stamp();
-      if (mode == 0) {
-        hist_to_counts(tot_p, HIST_LEV, s_tot);
-      } else {
-        load_totals(tot_p, 3, s_tot);
-      }
+      if (mode == 0) hist_to_counts(tot_p, HIST_LEV, s_tot);
+      else load_totals(tot_p, 3, s_tot);
       if (tid == 0) {
         if (mode == 0) {
           // counts are non-increasing in the key: binary search for the last key with >= k
@@ -1278,67 +1399,126 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       const uint32_t P = sc.prev_T;
       sc.prev_dT = (P > 0u) ? (T > P ? T - P : P - T) : (1u << 21);
       sc.prev_T = T;
+      // next call's ef-phase compaction key: below T by twice its last move plus a margin
+      const uint32_t delta = min(1u << 22, 2u * min(sc.prev_dT, 1u << 22) + (1u << 10));
+      sc.ef_key = T > delta ? T - delta : 0u;
     }
     __syncthreads();
   } else {
-  // ---- A3-A5: count passes.  The first resolves lev0 levels on the whole vector and compacts;
-  // when the compacted entries are exact for the rest, each further pass resolves up to HIST_LEV
-  // levels on them at once (histogram pass), else up to 2 levels per pass on the whole vector.
-  // The bits do not depend on this schedule. ----
+  // ---- A3-A5: count passes.  A search runs passes from slot p0 until N levels are resolved.
+  // fast: every pass is a histogram pass (up to HIST_LEV levels at once) over the ef-phase
+  // entries {a >= efk}.  A count is exact for a key >= efk and a lower bound below it, so a
+  // trial below efk can only err toward "nnz <= k" (hi := ratio), after which every later trial
+  // and the final l lie below that key.  Hence the search is exact (same decisions, k1, k2,
+  // thresholds, window and selection) iff thres2 ends up set with key2 >= efk - checked after
+  // the search, with a full restart on failure.  The logged nnz of a trial below efk is then a
+  // lower bound (> k); those trials are flagged in nnz_lb.  Otherwise the first
+  // pass counts lev0 levels on the whole vector and compacts; when those entries are exact for
+  // the rest, each further pass is a histogram pass on them, else it resolves up to 2 levels on
+  // the whole vector.  The bits do not depend on this schedule. ----
   const int N = (int)f.n_iters;
   __shared__ int s_got;
-  int done = 0;
-  for (int p = 0; done < N; ++p) {
-    int lev;
-    bool hist = false;
-    uint32_t* tot_p = f.totals + HIST_BINS * HREP * p;
-    if (p == 0) {
-      lev = f.lev0;  // keys along the predicted path
-      if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, 0);
-      else if (lev == 2) run_count<2, COUNT_FIRST>(f, &sc, 0);
-      else run_count<3, COUNT_FIRST>(f, &sc, 0);
-    } else if (sc.cap_ok) {
-      hist = true;
-      lev = min(min(HIST_LEV, f.cap_levels), N - done);
-      switch (lev) {
-        case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist); break;
-        case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist); break;
-        case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist); break;
-        case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist); break;
-        case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist); break;
-        case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist); break;
-        case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist); break;
-        default: hist_phase<8>(&sc, f.cp, tot_p, s_hist); break;
-      }
-    } else {
-      lev = min(min(2, f.cap_levels), N - done);
-      if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<3, COUNT_FULL>(f, &sc, p);
-    }
-    grid_sync(f.bar);
-    stamp();
-    if (hist) {
-      hist_to_counts(tot_p, lev, s_tot);
-    } else {
-      load_totals(tot_p, 16, s_tot);
-    }
-    if (tid == 0) {
-      const double cmp_ratio = sc.cmp_ratio;
-      s_got = replay_levels(&sc, s_tot, min(lev, N - done), p, f.sp.k);
-      if (p == 0) {
-        // compacted mode is exact iff every later threshold (and thres2) lies above the compaction
-        // key: the bracket's lower end must have reached its ratio, and nothing overflowed
-        sc.cap_ok = (sc.lo >= cmp_ratio && __ldcg(f.flags) == 0u) ? 1u : 0u;
-      }
-      if (done + s_got == N) finish_window(&sc, f.sp);
-    }
-    __syncthreads();
-    done += s_got;
-    if (done < N) {
-      const int next = sc.cap_ok ? min(min(HIST_LEV, f.cap_levels), N - done) : min(min(2, f.cap_levels), N - done);
-      make_candidates_par(&sc, next);
+  auto search = [&](int p0, bool fast) -> int {
+    int done = 0;
+    int p = p0;
+    if (fast) {
+      make_candidates_par(&sc, min(min(HIST_LEV, f.cap_levels), N));
       __syncthreads();
     }
+    for (; done < N; ++p) {
+      int lev;
+      bool hist = false;
+      uint32_t* tot_p = f.totals + HIST_BINS * HREP * p;
+      const bool first = (p == p0) && !fast;
+      if (first) {
+        lev = f.lev0;  // keys along the predicted path
+        if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, p);
+        else if (lev == 2) run_count<2, COUNT_FIRST>(f, &sc, p);
+        else run_count<3, COUNT_FIRST>(f, &sc, p);
+      } else if (sc.cap_ok) {
+        hist = true;
+        lev = min(min(HIST_LEV, f.cap_levels), N - done);
+        switch (lev) {
+          case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist); break;
+          case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist); break;
+          case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist); break;
+          case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist); break;
+          case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist); break;
+          case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist); break;
+          case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist); break;
+          default: hist_phase<8>(&sc, f.cp, tot_p, s_hist); break;
+        }
+      } else {
+        lev = min(min(2, f.cap_levels), N - done);
+        if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<3, COUNT_FULL>(f, &sc, p);
+      }
+      grid_sync(f.bar);
+      stamp();
+      if (hist) hist_to_counts(tot_p, lev, s_tot);
+      else load_totals(tot_p, 16, s_tot);
+      if (tid == 0) {
+        const double cmp_ratio = sc.cmp_ratio;
+        s_got = replay_levels(&sc, s_tot, min(lev, N - done), p, f.sp.k);
+        if (first) {
+          // compacted mode is exact iff every later threshold (and thres2) lies above the compaction
+          // key: the bracket's lower end must have reached its ratio, and nothing overflowed
+          sc.cap_ok = (sc.lo >= cmp_ratio && __ldcg(f.flags) == 0u) ? 1u : 0u;
+        }
+        if (done + s_got == N) finish_window(&sc, f.sp);
+      }
+      __syncthreads();
+      done += s_got;
+      if (done < N) {
+        const int next = sc.cap_ok ? min(min(HIST_LEV, f.cap_levels), N - done) : min(min(2, f.cap_levels), N - done);
+        make_candidates_par(&sc, next);
+        __syncthreads();
+      }
+    }
+    return p;
+  };
+  int pnext = 0;
+  bool ok = false;
+  if (ef_ok) {
+    if (tid == 0) { sc.cap_ok = 1u; sc.cmp_bottom = 1u; }
+    __syncthreads();
+    pnext = search(0, true);
+    if (tid == 0) {
+      s_got = (sc.prov2 >= 0 && sc.key2 >= efk) ? 1 : 0;
+      uint64_t lb = 0;
+      for (uint32_t i = 0; i < sc.it && i < (uint32_t)NMAX; ++i)
+        if (sc.key_log[i] < efk) lb |= 1ull << i;
+      sc.nnz_lb = s_got ? lb : 0ull;
+    }
+    __syncthreads();
+    ok = s_got != 0;
   }
+  if (!ok) {
+    if (tid == 0) {
+      search_reset(&sc, f.sp.n);
+      sc.nnz_lb = 0ull;
+      sc.cap_ok = 0u;
+      sc.cmp_bottom = 0u;
+      first_pass_candidates(&sc, f.lev0);
+    }
+    __syncthreads();
+    search(pnext, false);
+  }
+  if (tid == 0) {
+    sc.ef_used = ok ? 1u : 0u;
+    // next call's ef-phase compaction key: below this key2 by twice its last move plus a margin
+    const uint32_t K = sc.key2;
+    if (sc.prov2 >= 0) {
+      const uint32_t P = sc.prev_key2;
+      const uint32_t dk = (P > 0u) ? (K > P ? K - P : P - K) : (1u << 21);
+      const uint32_t margin = min(1u << 22, 2u * min(dk, 1u << 22) + (1u << 14));
+      sc.ef_key = K > margin ? K - margin : 0u;
+      sc.prev_key2 = K;
+    } else {
+      sc.ef_key = 0u;
+      sc.prev_key2 = 0u;
+    }
+  }
+  __syncthreads();
   }  // SEL_MSTOPK
   stamp();
   // ---- A7 prefix: class-1 / class-2 counts of each warp slab, then of the CTAs before it ----
@@ -1354,7 +1534,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     const int32_t k1m1 = sc.prov1 >= 0 ? (int32_t)sc.key1 - 1 : 0x7FFFFFFF;
     const int32_t k2m1 = (int32_t)sc.key2 - 1;
     const uint32_t ne = min(__ldcg(f.cp.cnt + gw), f.cp.C);
-    const uint32_t* eb = f.cp.bits + (size_t)gw * f.cp.C + (f.cp.C - ne);
+    const uint32_t* eb = f.cp.bits + (size_t)gw * f.cp.C + entry_off(f.cp, ne, sc.cmp_bottom);
     if (lane == 0) s_ne[warp] = ne;
 #pragma unroll 4
     for (uint32_t j = lane; j < ne; j += 32) {

@@ -119,3 +119,21 @@ def test_exact_flat_step_single_rank(tk, d, rho, dist):
 def test_exact_full_size_c2(tk):
     """BASELINE config 2's shape (d = 25.6M, rho = 1e-3, error feedback), two steps."""
     _case(tk, 25_600_000, "G", 25_600, steps=2, cfg=2)
+
+
+def test_exact_restart_on_shift(tk):
+    """scale jumps make the predicted compaction key useless (overflow / above T): still exact"""
+    d, k = 300_007, 300
+    ctx = tk.Context(d, k=k, select="exact")
+    r = np.zeros(d, np.float32)
+    rd = _dev(r)
+    used = set()
+    for step, sc in enumerate([1, 1, 1000, 1e-3, 1e-3, 1]):
+        g = (gradgen.gradient(d, "G", cfg=9, step=step) * np.float32(sc)).astype(np.float32)
+        idx, val = ctx.compress(_dev(g), rd)
+        ref = oracle.compress(g, r, k, 10, selector="exact")
+        _check(ctx, idx, val, rd, ref, True)
+        if step:
+            used.add(ctx.stats().ef_compacted)
+        r = ref.residual
+    assert used == {True, False}

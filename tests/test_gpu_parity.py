@@ -38,7 +38,11 @@ def _check_stats(st, ref):
     assert st.max_bits == int(np.float32(s.u).view(np.uint32))
     assert len(st.trials) == len(s.trials)
     for it, (a, b) in enumerate(zip(st.trials, s.trials)):
-        assert a[0] == b[0] and a[1] == b[1] and a[2] == b[2] and a[3] == b[3], (it, a, b)
+        assert a[0] == b[0] and a[1] == b[1] and a[2] == b[2], (it, a, b)
+        if st.nnz_lower_bound >> it & 1:  # below the EF-pass compaction key: a lower bound, > k
+            assert s.k < a[3] <= b[3], (it, a, b)
+        else:
+            assert a[3] == b[3], (it, a, b)
     assert (st.k1, st.k2) == (s.k1, s.k2)
     assert st.thres1_set == s.thres1_set and st.thres2_set == s.thres2_set
     assert st.thres1 == s.thres1 and st.thres2 == s.thres2
@@ -250,3 +254,54 @@ def test_compress_full_size_c3(tk):
         assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32))
         r = ref.residual
         ctx.set_step(step + 1)
+
+
+# ------------------------------------------------------------------ EF-pass compaction (predicted key)
+_EF_PATHS = set()
+
+
+def _multi_step(tk, d, dist, k, N, steps, *, scales=None, levels=0, seed=12, cfg=60):
+    """consecutive compressions on one context: from the second call on, the EF pass compacts at a
+    key predicted by the previous call; every call is compared with the oracle bit for bit"""
+    ctx = tk.Context(d, k=k, n_iters=N, seed=seed, levels_per_pass=levels)
+    r = np.zeros(d, np.float32)
+    rd = _dev(r)
+    for step in range(steps):
+        g = gradgen.gradient(d, dist, cfg=cfg, step=step)
+        if scales is not None:
+            g = (g * np.float32(scales[step])).astype(np.float32)
+        ctx.set_step(step)
+        idx, val = ctx.compress(_dev(g), rd)
+        ref = oracle.compress(g, r, k, N, seed=seed, step=step)
+        st = ctx.stats()
+        _check_stats(st, ref)
+        assert np.array_equal(_u32(idx), ref.sel.idx), step
+        assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32)), step
+        assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32)), step
+        if step > 0:
+            _EF_PATHS.add(st.ef_compacted)
+        r = ref.residual
+    ctx.close()
+
+
+@pytest.mark.parametrize("dist", ["G", "L", "H", "ties8", "spike"])
+@pytest.mark.parametrize("d,rho,N", [(300_001, 0.001, 10), (1_000_003, 0.01, 20), (65537, 0.001, 5)])
+def test_ef_compaction_multi_step(tk, dist, d, rho, N):
+    _multi_step(tk, d, dist, oracle.k_from_density(d, rho), N, 5)
+
+
+@pytest.mark.parametrize("levels", [1, 3, 8])
+def test_ef_compaction_levels(tk, levels):
+    _multi_step(tk, 200_003, "G", 200, 13, 4, levels=levels)
+
+
+def test_ef_compaction_restart_on_shift(tk):
+    # the scale jumps: the predicted key is far too low (entries overflow) or too high (a trial
+    # falls below it); both calls must restart the search and stay bit-exact
+    _multi_step(tk, 400_003, "G", 400, 10, 6, scales=[1, 1, 1000, 1e-3, 1e-3, 1])
+
+
+def test_ef_compaction_paths_exercised(tk):
+    _multi_step(tk, 100_003, "G", 100, 10, 3)
+    _multi_step(tk, 100_003, "G", 100, 10, 4, scales=[1, 1, 1e4, 1])
+    assert _EF_PATHS == {True, False}
