@@ -482,14 +482,31 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   const uint64_t u0 = (uint64_t)gw * units_per_warp;
   const bool cmp_on = ckey > 0u;
   const int32_t ckm1 = (int32_t)ckey - 1;
-  uint32_t ncomp = 0;
+  // hits are staged per warp in shared memory and written to the entries in coalesced runs
+  constexpr uint32_t SCAP = 256;
+  __shared__ uint32_t s_si[WARPS][SCAP], s_sb[WARPS][SCAP];
+  uint32_t staged = 0, flushed = 0;  // warp-uniform
   uint32_t* oi = cp.idx + (size_t)gw * cp.C;
   uint32_t* ob = cp.bits + (size_t)gw * cp.C;
+  auto flush = [&]() {
+    __syncwarp();
+    for (uint32_t j = lane; j < staged; j += 32)
+      if (flushed + j < cp.C) {
+        oi[flushed + j] = s_si[warp][j];
+        ob[flushed + j] = s_sb[warp][j];
+      }
+    flushed += staged;
+    staged = 0;
+    __syncwarp();
+  };
   double stk[24];
   uint32_t mx = 0;
   // NP == 0: the next unit's loads are issued before this unit is reduced (one unit in flight
   // ahead per warp); the peer-sum variant (NP > 0) keeps NP*4 loads per unit and no prefetch
-  constexpr bool PREF = false;  // measured: prefetching does not help this phase (it runs at ~94% of the copy peak)
+#ifndef TK_EF_PREF
+#define TK_EF_PREF 0
+#endif
+  constexpr bool PREF = TK_EF_PREF != 0;  // measured: prefetching does not help this phase
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 ng[4] = {z4, z4, z4, z4}, nr[4] = {z4, z4, z4, z4};
   bool nfull = units_per_warp > 0 && (u0 + 1) * ROUND <= n;
@@ -563,7 +580,12 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
         }
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t excl = incl - packed;
-        uint32_t cb = ncomp;
+        const uint32_t tu = (tot & 0xFFu) + ((tot >> 8) & 0xFFu) + ((tot >> 16) & 0xFFu) + (tot >> 24);
+        if (staged + tu > SCAP) flush();
+        // the unit's hits go to the warp's shared-memory staging buffer (or, if more than it
+        // holds, straight to the entries)
+        const bool direct = tu > SCAP;
+        uint32_t cb = direct ? flushed : staged;
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
           uint32_t pos = cb + ((excl >> (8 * ch)) & 0xFFu);
@@ -572,16 +594,20 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             if (m & (1u << (4 * ch + e))) {
-              if (pos < cp.C) {
-                oi[pos] = (uint32_t)(u * ROUND + ch * 128 + 4 * lane + e);
-                ob[pos] = w4[e];
+              const uint32_t i = (uint32_t)(u * ROUND + ch * 128 + 4 * lane + e);
+              if (direct) {
+                if (pos < cp.C) { oi[pos] = i; ob[pos] = w4[e]; }
+              } else {
+                s_si[warp][pos] = i;
+                s_sb[warp][pos] = w4[e];
               }
               ++pos;
             }
           }
           cb += (tot >> (8 * ch)) & 0xFFu;
         }
-        ncomp = cb;
+        if (direct) flushed += tu; else staged += tu;
+        __syncwarp();
       }
     }
     double cs[4];
@@ -598,6 +624,8 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
     for (uint32_t cnt = i; cnt & 1u; cnt >>= 1) v = __dadd_rn(stk[lvl++], v);  // binary-counter stack
     stk[lvl] = v;
   }
+  if (cmp_on) flush();
+  const uint32_t ncomp = flushed;
   int top = 0;
   while ((1u << top) < units_per_warp) ++top;
   mx = __reduce_max_sync(0xffffffffu, mx);
@@ -1399,8 +1427,10 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       const uint32_t P = sc.prev_T;
       sc.prev_dT = (P > 0u) ? (T > P ? T - P : P - T) : (1u << 21);
       sc.prev_T = T;
-      // next call's ef-phase compaction key: below T by twice its last move plus a margin
-      const uint32_t delta = min(1u << 22, 2u * min(sc.prev_dT, 1u << 22) + (1u << 10));
+      // next call's ef-phase compaction key: below T by half its last move if T rose (error
+      // feedback grows the residual), else twice it, plus a margin
+      const uint32_t mv = min(sc.prev_dT, 1u << 22);
+      const uint32_t delta = min(1u << 22, ((P > 0u && T > P) ? mv / 2u : 2u * mv) + (1u << 10));
       sc.ef_key = T > delta ? T - delta : 0u;
     }
     __syncthreads();
@@ -1510,7 +1540,10 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     if (sc.prov2 >= 0) {
       const uint32_t P = sc.prev_key2;
       const uint32_t dk = (P > 0u) ? (K > P ? K - P : P - K) : (1u << 21);
-      const uint32_t margin = min(1u << 22, 2u * min(dk, 1u << 22) + (1u << 14));
+      // a rising key2 (error feedback grows the residual) is expected to keep rising: half the
+      // last move below it; a falling one: twice the last move
+      const uint32_t mv = min(dk, 1u << 22);
+      const uint32_t margin = min(1u << 22, ((P > 0u && K > P) ? mv / 2u : 2u * mv) + (1u << 12));
       sc.ef_key = K > margin ? K - margin : 0u;
       sc.prev_key2 = K;
     } else {
