@@ -407,7 +407,7 @@ def main():
                 "config": {"workload": workload_name(a, P), "d": a.d, "rho": a.rho, "k": k, "n_iters": a.n_iters,
                            "P": P, "group_size": n, "step4": a.step4 if n > 1 else None, "dist": a.dist,
                            "allgather": (a.ag_mode if n == 1 and P > 1 else None), "selector": a.select,
-                           "levels_per_pass": a.levels or 4, "input_buffers": nbuf,
+                           "levels_per_pass": a.levels or 10, "input_buffers": nbuf,
                            "inputs": "fresh seeded N(0,1) gradient per step (torch CUDA generator, pre-generated in "
                                      "HBM); residual carried from r=0 at step 0; timed steps W..W+K-1",
                            "l2": "inputs larger than L2: each step reads a fresh g (4d B) and touches r and out: "

@@ -82,7 +82,7 @@ typedef struct tk_config {
   uint32_t error_feedback; /* 1: acc = g + r, r' = acc with sent entries := +0.0 (Q14);
                               0: MSTopK runs on g itself and r is ignored (may be NULL)         */
   uint32_t step4;          /* HiTopKComm step 4 mode (TK_STEP4_DENSE or TK_STEP4_SPARSE)       */
-  uint32_t levels_per_pass;/* bisection levels resolved per count pass (1..8; 0 = default 8): the
+  uint32_t levels_per_pass;/* bisection levels resolved per count pass (1..10; 0 = default 10): the
                               first pass over the whole vector resolves min(2, this); later passes
                               on the compacted entries resolve up to this many at once, passes
                               over the whole vector up to 2.  Result bits do not depend on it.  */

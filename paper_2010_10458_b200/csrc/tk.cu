@@ -361,7 +361,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if (k.k == 0 && (!(k.rho > 0.0) || k.rho > 1.0)) return TK_ERR_INVALID_ARG;
   if (k.n_iters < 1 || k.n_iters > (uint32_t)NMAX) return TK_ERR_INVALID_ARG;
   if (k.nranks < 1 || k.rank >= k.nranks) return TK_ERR_INVALID_ARG;
-  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 8 || k.rs_mode > 1 ||
+  if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 10 || k.rs_mode > 1 ||
       k.ag_mode > 1 || k.select > 1)
     return TK_ERR_INVALID_ARG;
   const uint32_t n = k.group_size == 0 ? 1 : k.group_size;
@@ -390,7 +390,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   c->L = L;
   c->k = kk;
   c->stream = reinterpret_cast<cudaStream_t>(stream);
-  c->levels = k.levels_per_pass == 0 ? 8 : k.levels_per_pass;
+  c->levels = k.levels_per_pass == 0 ? 10 : k.levels_per_pass;
   // pass schedule (decided on the device): the first pass resolves min(2, levels) levels on the
   // whole vector; later passes take up to `levels` levels on the compacted entries, or up to 2 on
   // the whole vector.  Scratch is sized for the worst case (all passes on the whole vector).

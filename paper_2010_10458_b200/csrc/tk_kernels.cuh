@@ -25,7 +25,11 @@ constexpr uint32_t NO_INDEX = 0xFFFFFFFFu;
 // Global pass totals / histograms are replicated HREP times (copy = CTA index mod HREP) so the
 // CTAs' atomic adds spread over HREP addresses per bin; readers sum the copies.
 constexpr int HREP = 8;
-constexpr int TOT_STRIDE = 256;  // words per copy (= HIST_BINS)
+// COUNT_HIST: up to HIST_LEV bisection levels (2^HIST_LEV - 1 candidate keys) per histogram pass
+constexpr int HIST_LEV = 10;
+constexpr int HIST_BINS = 1 << HIST_LEV;
+constexpr int TOT_STRIDE = HIST_BINS;  // words per copy
+constexpr int NPATH_CAND = 16;           // candidates with an explicit ratio / threshold (path, exact)
 
 // Device-resident MSTopK control block (Alg. 1 l.4-6 state + the trial log).
 struct Ctrl {
@@ -40,9 +44,9 @@ struct Ctrl {
   int32_t prov1, prov2;  // slot (pass*TMAX + candidate) whose per-warp counts are key1's / key2's; -1 unset
   uint32_t it;           // trials done
   uint32_t ncand;        // candidates of the pass about to run
-  uint32_t cand_key[256];
-  double cand_ratio[256];
-  double cand_t[256];
+  uint32_t cand_key[HIST_BINS];  // candidate keys (ascending for a tree / histogram pass)
+  double cand_ratio[NPATH_CAND];    // ratio / threshold of path candidates (tree candidates are
+  double cand_t[NPATH_CAND];        // recomputed from lo, hi in the replay)
   uint32_t ticket;
   uint32_t cap_ok;       // 1: passes >= 1 and the selection run on the compacted entries (see k_count)
   uint32_t cmp_key;      // key above which the first count pass compacts elements
@@ -198,15 +202,11 @@ __device__ __forceinline__ uint32_t key_of(double t) {
 // Computed by the CTA's threads in parallel (candidate m-1 by thread m-1); the caller
 // synchronises the CTA before and after.
 __device__ void make_candidates_par(Ctrl* c, int lev) {
-  const int T = (1 << lev) - 1;  // <= 255: one candidate per thread
-  const int m = (int)threadIdx.x + 1;
-  if (m <= T) {
-    const double w = __dsub_rn(c->hi, c->lo);
+  const int T = (1 << lev) - 1;  // <= 1023
+  const double w = __dsub_rn(c->hi, c->lo);
+  for (int m = (int)threadIdx.x + 1; m <= T; m += THREADS) {
     const double ratio = __dadd_rn(c->lo, __dmul_rn(w, (double)m * ldexp(1.0, -lev)));
-    const double t = threshold_of(c->abar, c->U, ratio);
-    c->cand_ratio[m - 1] = ratio;
-    c->cand_t[m - 1] = t;
-    c->cand_key[m - 1] = key_of(t);
+    c->cand_key[m - 1] = key_of(threshold_of(c->abar, c->U, ratio));
   }
   if (threadIdx.x == 0) {
     c->ncand = (uint32_t)T;
@@ -228,15 +228,19 @@ __device__ int replay_levels(Ctrl* c, const uint32_t* totals, int max_lev, int p
   for (; l < max_lev; ++l) {
     const double ratio = __dadd_rn(c->lo, __dmul_rn(__dsub_rn(c->hi, c->lo), 0.5));  // Alg. 1 l.8
     int s = -1;
+    double t;
     if (tree) {
-      if (m >= 1 && m <= nc && c->cand_ratio[m - 1] == ratio) s = m - 1;
+      // node m of the complete subtree is exactly this level's midpoint (dyadic, Q5): its
+      // threshold and key are recomputed by the same operations make_candidates_par used
+      if (m >= 1 && m <= nc) s = m - 1;
+      t = threshold_of(c->abar, c->U, ratio);
     } else {
-      for (int q = 0; q < nc; ++q)
+      for (int q = 0; q < nc && q < NPATH_CAND; ++q)
         if (c->cand_ratio[q] == ratio) { s = q; break; }
+      t = s >= 0 ? c->cand_t[s] : 0.0;
     }
     if (s < 0) break;
     const uint32_t nnz = totals[s];
-    const double t = c->cand_t[s];
     const uint32_t key = c->cand_key[s];
     const uint32_t it = c->it;
     c->ratio_log[it] = ratio;
@@ -894,23 +898,17 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
 // candidate keys sit in shared memory; each entry finds its bucket b = #{s : key_s <= a} by a
 // LEV-step binary search and bumps a per-warp shared-memory histogram; the CTA histogram is added
 // to the pass's global histogram; after the barrier nnz_s = sum_{b > s} hist[b] (exact).
-constexpr int HIST_LEV = 8;
-constexpr int HIST_BINS = 1 << HIST_LEV;
-
 struct HistSmem {
-  int32_t key[HIST_BINS];
-  uint32_t h[WARPS][HIST_BINS];
+  uint32_t h[HIST_BINS];  // the CTA's histogram (shared-memory atomics; entries spread over the bins)
 };
 
 template <int LEV>
 __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uint32_t* ghist, HistSmem& hs) {
-  constexpr int T = (1 << LEV) - 1;
   constexpr int NB = 1 << LEV;
-  int32_t* s_key = hs.key;
-  auto& s_h = hs.h;
+  const int32_t* s_key = reinterpret_cast<const int32_t*>(sc->cand_key);  // sorted, in shared memory
+  uint32_t* s_h = hs.h;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < T; i += THREADS) s_key[i] = (int32_t)sc->cand_key[i];
-  for (int i = lane; i < NB; i += 32) s_h[warp][i] = 0u;
+  for (int i = threadIdx.x; i < NB; i += THREADS) s_h[i] = 0u;
   __syncthreads();
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
@@ -920,7 +918,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
     uint32_t b = 0;
 #pragma unroll
     for (int l = LEV - 1; l >= 0; --l) b += (a >= s_key[b + (1u << l) - 1]) ? (1u << l) : 0u;
-    atomicAdd(&s_h[warp][b], 1u);
+    atomicAdd(&s_h[b], 1u);
   };
   for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
     uint4 q[4];
@@ -942,9 +940,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
   }
   __syncthreads();
   for (int b = threadIdx.x; b < NB; b += THREADS) {
-    uint32_t t = 0;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) t += s_h[w][b];
+    const uint32_t t = s_h[b];
     if (b > 0 && t) atomicAdd(ghist + (blockIdx.x & (HREP - 1)) * TOT_STRIDE + b, t);  // bucket 0 is never needed
   }
   __syncthreads();
@@ -960,18 +956,29 @@ __device__ __forceinline__ void load_totals(const uint32_t* tot_p, int nk, uint3
   __syncthreads();
 }
 
-// nnz of every candidate from the global histogram: nnz_s = sum_{b >= s+1} hist[b]
+// nnz of every candidate from the global histogram: nnz_s = sum_{b >= s+1} hist[b].  Thread t
+// owns the reversed positions 4t..4t+3 (bins NB-1-4t .. NB-4-4t); a block scan of the thread
+// sums gives the suffix sums.
 __device__ __forceinline__ void hist_to_counts(const uint32_t* ghist, int lev, uint32_t* s_tot) {
   __shared__ uint32_t s_w[WARPS];
   const int NB = 1 << lev;
-  // thread t owns bin NB-1-t (a reversed inclusive scan gives the suffix sums)
-  const int b = NB - 1 - (int)threadIdx.x;
-  uint32_t v = 0u;
-  if (b >= 1)
-    for (int c = 0; c < HREP; ++c) v += __ldcg(ghist + c * TOT_STRIDE + b);
+  uint32_t v[4], sum = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int b = NB - 1 - (4 * (int)threadIdx.x + q);
+    v[q] = 0u;
+    if (b >= 1)
+      for (int c = 0; c < HREP; ++c) v[q] += __ldcg(ghist + c * TOT_STRIDE + b);
+    sum += v[q];
+  }
   uint32_t total;
-  const uint32_t excl = block_excl_scan(v, s_w, total);
-  if (b >= 1) s_tot[b - 1] = excl + v;  // sum over bins b..NB-1 = nnz of candidate b-1
+  uint32_t acc = block_excl_scan(sum, s_w, total);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int b = NB - 1 - (4 * (int)threadIdx.x + q);
+    acc += v[q];
+    if (b >= 1) s_tot[b - 1] = acc;  // sum over bins b..NB-1 = nnz of candidate b-1
+  }
   __syncthreads();
 }
 
@@ -1345,7 +1352,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       uint32_t* tot_p = f.totals + HIST_BINS * HREP * p;
       if (tid == 0) {
         if (sc.cap_ok) {
-          s_mode = 0;  // histogram of the compacted entries over 255 keys splitting the bracket
+          s_mode = 0;  // histogram of the compacted entries over 1023 keys splitting the bracket
         } else if (!sc.xretry && (uint64_t)sc.xcnt_lo * 8u <= f.sp.n) {
           s_mode = 1;  // compact again at xlo (<= T, so exact unless a warp overflows)
           sc.xretry = 1u;
@@ -1356,7 +1363,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       __syncthreads();
       const int mode = s_mode;
       if (mode == 0) {
-        if (tid < HIST_BINS - 1) sc.cand_key[tid] = exact_split(&sc, tid + 1, HIST_BINS);
+        for (int j = tid; j < HIST_BINS - 1; j += THREADS) sc.cand_key[j] = exact_split(&sc, j + 1, HIST_BINS);
         __syncthreads();
         hist_phase<HIST_LEV>(&sc, f.cp, tot_p, s_hist);
       } else {
@@ -1383,7 +1390,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       if (tid == 0) {
         if (mode == 0) {
           // counts are non-increasing in the key: binary search for the last key with >= k
-          int lo = -1, hi = HIST_BINS - 1;  // s_tot[lo] >= k (lo = -1: none), s_tot[hi] < k (hi = 255: none)
+          int lo = -1, hi = HIST_BINS - 1;  // s_tot[lo] >= k (lo = -1: none), s_tot[hi] < k (hi = 1023: none)
           while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if ((uint64_t)s_tot[mid] >= k) lo = mid; else hi = mid;
@@ -1476,7 +1483,9 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
           case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist); break;
           case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist); break;
           case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist); break;
-          default: hist_phase<8>(&sc, f.cp, tot_p, s_hist); break;
+          case 8: hist_phase<8>(&sc, f.cp, tot_p, s_hist); break;
+          case 9: hist_phase<9>(&sc, f.cp, tot_p, s_hist); break;
+          default: hist_phase<10>(&sc, f.cp, tot_p, s_hist); break;
         }
       } else {
         lev = min(min(2, f.cap_levels), N - done);
@@ -1486,6 +1495,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       stamp();
       if (hist) hist_to_counts(tot_p, lev, s_tot);
       else load_totals(tot_p, 16, s_tot);
+      if (fast) stamp();
       if (tid == 0) {
         const double cmp_ratio = sc.cmp_ratio;
         s_got = replay_levels(&sc, s_tot, min(lev, N - done), p, f.sp.k);
@@ -1497,6 +1507,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         if (done + s_got == N) finish_window(&sc, f.sp);
       }
       __syncthreads();
+      if (fast) stamp();
       done += s_got;
       if (done < N) {
         const int next = sc.cap_ok ? min(min(HIST_LEV, f.cap_levels), N - done) : min(min(2, f.cap_levels), N - done);

@@ -82,7 +82,7 @@ def test_init_rejects_bad_config_before_touching_the_gpu():
     assert init(d=1001, nranks=2, group_size=2) == 3  # d % n != 0
     assert init(d=1004, nranks=4, group_size=4) == 3  # (d / n) % 4 != 0: unaligned segments
     assert init(k=1001) == 2                      # k > d
-    assert init(levels_per_pass=9) == 1
+    assert init(levels_per_pass=11) == 1
 
 
 def test_product_has_no_cpu_path():

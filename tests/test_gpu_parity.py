@@ -92,7 +92,7 @@ def test_compress_distributions(tk, dist, d, rho, N):
     _compress_case(tk, d, dist, oracle.k_from_density(d, rho), N, seed=3, step=1, r_scale=0.05)
 
 
-@pytest.mark.parametrize("levels", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("levels", [1, 2, 3, 4, 5, 8, 9, 10])
 @pytest.mark.parametrize("N", [1, 2, 3, 7, 10, 13, 30, 52])
 def test_compress_levels_per_pass_invariance(tk, levels, N):
     _compress_case(tk, 50003, "L", 50, N, levels=levels, seed=5)

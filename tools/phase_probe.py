@@ -22,6 +22,8 @@ for s in range(steps):
         acc = st.phase_us if acc is None else [a + b for a, b in zip(acc, st.phase_us)]
 n = steps - 20
 names = ["ef", "root"] + [f"pass{i}" for i in range(len(acc) - 5)] + ["replay", "prefix", "select"]
+if st.ef_compacted and select == "mstopk":  # fast search: pass, counts, replay per pass, then verify
+    names = ["ef", "root"] + sum([[f"pass{i}", f"counts{i}", f"replay{i}"] for i in range((len(acc) - 4) // 3)], []) + ["verify", "prefix", "select"]
 if select == "exact":
     names = ["ef", "root"] + [f"pass{i}" for i in range(len(acc) - 4)] + ["prefix", "select"]
 print(select, "phases (us):", {names[i] if i < len(names) else i: round(v / n, 1) for i, v in enumerate(acc)},
