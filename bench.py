@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--step4", default="dense", choices=["dense", "sparse"])
     ap.add_argument("--levels", type=int, default=0, help="bisection levels per count pass (0 = default)")
     ap.add_argument("--ag-mode", default="push", choices=["push", "nccl"], help="flat all-gather: fused peer push or NCCL")
+    ap.add_argument("--rs-mode", default="ordered", choices=["ordered", "nccl"],
+                    help="HiTopKComm step-1 reduce-scatter: ordered peer reads (bit-exact) or NCCL")
     ap.add_argument("--select", default="mstopk", choices=["mstopk", "exact"],
                     help="selector: MSTopK (Alg. 1) or the exact top-k of Eq. 2 (SURVEY F1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -274,7 +276,7 @@ def main():
     stream = torch.cuda.Stream()
     ctx = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, nranks=P, rank=rank, group_size=n, seed=2010_10458,
                      step4=a.step4, levels_per_pass=a.levels, uid=uid, stream=stream, device=local, ag_mode=a.ag_mode,
-                     select=a.select)
+                     select=a.select, rs_mode=a.rs_mode)
     L, k = ctx.seg_len, ctx.k
     log("ctx up")
     # inputs: a fresh seeded N(0,1) gradient for every warm-up / timed / profiled step, generated on

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <type_traits>
 #include <vector>
 
 #include "tk.h"
@@ -36,6 +37,7 @@ struct tk_ctx {
   uint64_t S = 0;                     // slab length
   uint32_t occ_dec = 1;               // resident decompression CTAs per SM
   uint32_t levels = 4, npass = 0;
+  uint32_t debug_check = 0;           // TK_CHECK=1: verify every selection (ascending, in range) on the device
   uint32_t ef_compact = 1;            // compaction in the ef phase (TK_EF_COMPACT=0 disables; bits unchanged)
   int lev_sched[NMAX];
   uint32_t units_per_warp = 1;        // ef phase: aligned power-of-two run of 512-element units per warp
@@ -186,11 +188,17 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.lev0 = c->lev_sched[0];
   f.cap_levels = (int)c->levels;
   f.max_pass = (int)c->npass;
-  f.ef_compact = c->ef_compact;
+  // EF-pass compaction is off when the EF pass sums peer segments (HiTopKComm ordered
+  // reduce-scatter): with it on, 1 in ~6 4-GPU bench runs hit an illegal address that no device
+  // check, launch-blocking or sanitised run reproduces (open issues)
+  f.ef_compact = (np == 0) ? c->ef_compact : 0u;
   const void* kern = compress_kernel(ef, np, c->cfg.select);
   if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
   void* args[] = {&f};
   TK_CUDA(c, cudaLaunchCooperativeKernel(kern, dim3(c->grid), dim3(THREADS), args, 0, c->stream));
+  if (c->debug_check) {
+    k_check_sel<<<1, 1024, 0, c->stream>>>(idx, c->k, c->L, (uint32_t)c->rank, (uint32_t)c->step, 0u);
+  }
   TK_TRY(check_launch(c, "k_compress"));
   mark(c, TK_STAGE_COMPRESS);
   return TK_OK;
@@ -205,6 +213,12 @@ tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t 
   const uint32_t max_cta = c->sms * c->occ_dec;
   const uint32_t per = (nt + max_cta - 1) / max_cta;
   const uint32_t grid = (nt + per - 1) / per;
+  if (c->debug_check) {
+    if constexpr (std::is_same<Src, PlainChunks>::value)
+      for (uint32_t p = 0; p < nchunks; ++p)
+        k_check_sel<<<1, 1024, 0, c->stream>>>(src.g + (size_t)p * 2 * kk, kk, len, (uint32_t)c->rank, (uint32_t)c->step,
+                                               1u + p);
+  }
   k_decompress<Src><<<grid, THREADS, sizeof(uint32_t) * nchunks, c->stream>>>(src, nchunks, kk, len, nt, per, out,
                                                                                plain_out);
   TK_TRY(check_launch(c, "k_decompress"));
@@ -407,6 +421,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
     if (k.select == TK_SELECT_EXACT) c->npass = 24;
     else c->npass += k.n_iters;  // an ef-phase search (>= 1 level per pass) may precede a restart
     if (const char* e = getenv("TK_EF_COMPACT")) c->ef_compact = atoi(e) != 0 ? 1u : 0u;
+    if (const char* e = getenv("TK_CHECK")) c->debug_check = atoi(e) != 0 ? 1u : 0u;
   }
   auto bail = [&](tk_status s) {
     free_all(c);

@@ -22,6 +22,18 @@ constexpr int TMAX = 15;            // max candidates per count pass (4 bisectio
 constexpr int NMAX = 52;            // max MSTopK samplings (Q5)
 constexpr uint32_t INF_BITS = 0x7F800000u;
 constexpr uint32_t NO_INDEX = 0xFFFFFFFFu;
+#ifdef TK_DEVICE_CHECKS
+#define TK_DCHECK(cond, tag, a, b)                                                                     \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("TK_DCHECK %s failed: blk %d thr %d a=%llu b=%llu\n", tag, (int)blockIdx.x, (int)threadIdx.x, \
+             (unsigned long long)(a), (unsigned long long)(b));                                       \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define TK_DCHECK(cond, tag, a, b) do { } while (0)
+#endif
 // Global pass totals / histograms are replicated HREP times (copy = CTA index mod HREP) so the
 // CTAs' atomic adds spread over HREP addresses per bin; readers sum the copies.
 constexpr int HREP = 8;
@@ -602,6 +614,7 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
               if (direct) {
                 if (pos < cp.C) { oi[pos] = i; ob[pos] = w4[e]; }
               } else {
+                TK_DCHECK(pos < SCAP, "ef-stage", pos, staged);
                 s_si[warp][pos] = i;
                 s_sb[warp][pos] = w4[e];
               }
@@ -1051,12 +1064,14 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
         if (fc1 & (1u << e)) {
           const uint32_t after = (q2 > rnd) ? min(q2 - rnd, need) : 0u;
           const uint32_t pos = q1 + after;
+          TK_DCHECK(pos < sp.k && ii[e] < sp.n, "sel-cap1", pos, ii[e]);
           { idx_out[pos] = ii[e]; val_out[pos] = __uint_as_float(bb[e]); }
           if (r_zero) r_zero[ii[e]] = 0.0f;
           ++q1;
         } else if (fc2 & (1u << e)) {
           if (q2 >= rnd && q2 < rnd + need) {
             const uint32_t pos = q1 + (q2 - rnd);
+            TK_DCHECK(pos < sp.k && ii[e] < sp.n, "sel-cap2", pos, ii[e]);
             { idx_out[pos] = ii[e]; val_out[pos] = __uint_as_float(bb[e]); }
             if (r_zero) r_zero[ii[e]] = 0.0f;
           }
@@ -1101,12 +1116,14 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
         if (fc1 & (1u << e)) {
           const uint32_t after = (q2 > rnd) ? min(q2 - rnd, need) : 0u;
           const uint32_t pos = q1 + after;
+          TK_DCHECK(pos < sp.k && i < sp.n, "sel-full1", pos, i);
           { idx_out[pos] = i; val_out[pos] = __uint_as_float(__ldg(a32 + i)); }
           if (r_zero) r_zero[i] = 0.0f;
           ++q1;
         } else {
           if (q2 >= rnd && q2 < rnd + need) {
             const uint32_t pos = q1 + (q2 - rnd);
+            TK_DCHECK(pos < sp.k && i < sp.n, "sel-full2", pos, i);
             { idx_out[pos] = i; val_out[pos] = __uint_as_float(__ldg(a32 + i)); }
             if (r_zero) r_zero[i] = 0.0f;
           }
@@ -1738,6 +1755,7 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
         uint32_t c0;
         if (p < WARPS) {
           if (pi < thi) {
+            TK_DCHECK(pi >= tlo, "dec-pre", pi, tlo);
             s_tile[pi - tlo] = __fadd_rn(s_tile[pi - tlo], pv);
             emit(p, cur + lane, pi, pv);
           }
@@ -1753,6 +1771,7 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
             if (j < k) src.get(p, j, i, v);
             const bool in = i < thi;
             if (in) {
+              TK_DCHECK(i >= tlo, "dec-loop", i, tlo);
               s_tile[i - tlo] = __fadd_rn(s_tile[i - tlo], v);
               emit(p, j, i, v);
             }
@@ -1773,6 +1792,19 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
         if ((uint64_t)tlo + q < n) out[tlo + q] = s_tile[q];
     }
     __syncthreads();  // s_tile is rewritten by the next tile
+  }
+}
+
+// Debug (TK_CHECK=1): a selection / gathered chunk must hold strictly ascending indices < n.
+__global__ void k_check_sel(const uint32_t* idx, uint64_t k, uint64_t n, uint32_t rank, uint32_t step, uint32_t where) {
+  for (uint64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    const uint32_t i = idx[j];
+    const bool bad = i >= n || (j > 0 && idx[j - 1] >= i);
+    if (bad) {
+      printf("TK_CHECK rank %u step %u where %u: j=%llu idx=%u prev=%u n=%llu k=%llu\n", rank, step, where,
+             (unsigned long long)j, i, j > 0 ? idx[j - 1] : 0u, (unsigned long long)n, (unsigned long long)k);
+      __trap();
+    }
   }
 }
 
