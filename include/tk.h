@@ -161,6 +161,18 @@ tk_status tk_decompress(tk_ctx* ctx, const uint32_t* gathered, uint32_t nchunks,
  * Increments the step counter after enqueueing. */
 tk_status tk_step(tk_ctx* ctx, const float* g, float* r, float* out, uint32_t* gathered);
 
+/* tk_step followed by the SGD update of Eq. 1, w_{t+1} = w_t - lr * (aggregated sparse
+ * gradient), fused into the decompression's tile write-back: for every i,
+ * w[i] := fl32(w[i] - fl32(lr * out[i])) (two round-to-nearest fp32 operations, no FMA; Q29).
+ *   w   [d]   in/out  parameters (device, 16-byte aligned, replicated: identical on every rank)
+ *   lr          in     learning rate (finite)
+ *   out [d]   out     optional (NULL: the aggregate is not stored - flat and sparse-step-4
+ *                      HiTopKComm never write it; dense step 4 uses an internal buffer and applies
+ *                      the update after the row all-gather)
+ *   g, r, gathered as for tk_step.  w must not alias g, r or out.  TK_ERR_INVALID_ARG on a NULL or
+ *   misaligned w or a non-finite lr. */
+tk_status tk_step_sgd(tk_ctx* ctx, const float* g, float* r, float* w, float lr, float* out, uint32_t* gathered);
+
 /* tk_step with HOST buffers (end-to-end path): copies g_host (pinned or pageable) to the device,
  * runs tk_step with a context-owned device residual (state carried across calls; zero at init),
  * and copies the P*2k gathered pairs (flat) back to gathered_host and, if out_host != NULL, the

@@ -105,3 +105,11 @@ def hitopk_step(grads: list, residuals: list, m: int, n: int, rho: float, n_iter
         G.append(decompress(gathered, m, kt, L))  # Alg. 2 l.15-20, groups in order (Q16, Q18)
     out = np.concatenate(G)  # Alg. 2 l.21-23: intra-node All-Gather of segments (Q18, Q19)
     return HiTopKResult(out=out, segments=segs, per_rank=per, column_gathered=col)
+
+
+def sgd_update(w: np.ndarray, out: np.ndarray, lr: float) -> np.ndarray:
+    """Eq. 1 with the sparse aggregate in place of sum_p g_t^p:
+    w_{t+1} = w_t - eta * g~, elementwise in fp32: fl32(w - fl32(eta * g~)) (reading Q29)."""
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    prod = (np.float32(lr) * np.ascontiguousarray(out, dtype=np.float32)).astype(np.float32)
+    return (w - prod).astype(np.float32)

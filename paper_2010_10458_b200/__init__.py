@@ -61,7 +61,7 @@ class _Stats(ctypes.Structure):
 EXPORTS = ["tk_k", "tk_get_unique_id", "tk_init", "tk_compress", "tk_sparse_allgather", "tk_decompress",
            "tk_step", "tk_step_host", "tk_get_stats", "tk_set_step", "tk_query", "tk_launch_count",
            "tk_destroy", "tk_status_string", "tk_last_error", "tk_profile_begin", "tk_profile_end",
-           "tk_stage_name", "tk_input_buffer"]
+           "tk_stage_name", "tk_input_buffer", "tk_step_sgd"]
 NSTAGES = 16
 
 
@@ -79,6 +79,7 @@ def _load():
         "tk_sparse_allgather": (I32, [P, P, P, P]),
         "tk_decompress": (I32, [P, P, U32, P]),
         "tk_step": (I32, [P, P, P, P, P]),
+        "tk_step_sgd": (I32, [P, P, P, P, ctypes.c_float, P, P]),
         "tk_step_host": (I32, [P, P, P, P]),
         "tk_get_stats": (I32, [P, ctypes.POINTER(_Stats)]),
         "tk_set_step": (I32, [P, U64]),
@@ -268,6 +269,16 @@ class Context:
                                  _ptr(out, "out", torch.float32),
                                  _ptr(gathered, "gathered", torch.int32) if gathered is not None else None))
         return out
+
+    def step_sgd(self, g, r, w, lr: float, out=None, gathered=None):
+        """tk_step_sgd: one iteration plus Eq. 1's update w -= lr * aggregate, fused into the
+        decompression; w is updated in place (out optional)."""
+        self._check(_lib.tk_step_sgd(self._ctx, _ptr(g, "g", torch.float32),
+                                     _ptr(r, "r", torch.float32) if self.error_feedback else None,
+                                     _ptr(w, "w", torch.float32), ctypes.c_float(lr),
+                                     _ptr(out, "out", torch.float32) if out is not None else None,
+                                     _ptr(gathered, "gathered", torch.int32) if gathered is not None else None))
+        return w
 
     def step_host(self, g_host, gathered_host=None, out_host=None):
         """tk_step_host: HOST buffers in/out (numpy or pinned CPU tensors); synchronous."""

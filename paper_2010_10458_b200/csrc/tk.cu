@@ -208,7 +208,7 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
 // (fused all-gather) from tagged packets, optionally re-emitting the pairs in the plain layout.
 template <class Src>
 tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t kk, uint64_t len, float* out,
-                          uint32_t* plain_out = nullptr) {
+                          uint32_t* plain_out = nullptr, float* w = nullptr, float lr = 0.0f) {
   const uint32_t nt = (uint32_t)((len + TILE - 1) / TILE);
   const uint32_t max_cta = c->sms * c->occ_dec;
   const uint32_t per = (nt + max_cta - 1) / max_cta;
@@ -220,7 +220,7 @@ tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t 
                                                1u + p);
   }
   k_decompress<Src><<<grid, THREADS, sizeof(uint32_t) * nchunks, c->stream>>>(src, nchunks, kk, len, nt, per, out,
-                                                                               plain_out);
+                                                                               plain_out, w, lr);
   TK_TRY(check_launch(c, "k_decompress"));
   mark(c, TK_STAGE_DECOMPRESS);
   return TK_OK;
@@ -507,12 +507,17 @@ tk_status tk_decompress(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, f
   return decompress_impl(c, PlainChunks{gathered, c->k}, nchunks, c->k, len, out);
 }
 
-tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gathered) {
-  if (!c) return TK_ERR_INVALID_ARG;
+// One iteration (tk_step / tk_step_sgd).  w != nullptr: Eq. 1's update fused into the final
+// decompression (out may then be nullptr, except for HiTopKComm dense step 4, which needs it).
+static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gathered, float* w, float lr) {
   const bool ef = c->cfg.error_feedback != 0;
-  if (!g || !out || (ef && !r)) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
-  if (!aligned16(g) || !aligned16(out) || (ef && !aligned16(r))) return fail(c, TK_ERR_INVALID_ARG, "misaligned pointer");
-  if ((const void*)g == (const void*)r || (const void*)g == (const void*)out || (const void*)r == (const void*)out)
+  if (!g || (!out && !w) || (ef && !r)) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  if (w && !aligned16(w)) return fail(c, TK_ERR_INVALID_ARG, "misaligned w");
+  if (w && ((const void*)w == (const void*)g || (const void*)w == (const void*)r || (const void*)w == (const void*)out))
+    return fail(c, TK_ERR_INVALID_ARG, "w must not alias g, r or out");
+  if (!aligned16(g) || (out && !aligned16(out)) || (ef && !aligned16(r)))
+    return fail(c, TK_ERR_INVALID_ARG, "misaligned pointer");
+  if ((const void*)g == (const void*)r || (out && ((const void*)g == (const void*)out || (const void*)r == (const void*)out)))
     return fail(c, TK_ERR_INVALID_ARG, "g, r and out must not alias");
   mark(c, TK_STAGE_NONE);
   if (c->n == 1) {
@@ -539,12 +544,12 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
       c->push_seq++;
       mark(c, TK_STAGE_ALLGATHER);
       TaggedChunks src{c->pg + parity * stride, c->k, po.tag};
-      TK_TRY(decompress_impl(c, src, c->P, c->k, c->d, out, gat));
+      TK_TRY(decompress_impl(c, src, c->P, c->k, c->d, out, gat, w, lr));
     } else {
       TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k)));
       if (c->P > 1) TK_NCCL(c, ncclAllGather(mine, gat, 2 * c->k, ncclUint32, c->world, c->stream));
       mark(c, TK_STAGE_ALLGATHER);
-      TK_TRY(decompress_impl(c, PlainChunks{gat, c->k}, c->P, c->k, c->d, out));
+      TK_TRY(decompress_impl(c, PlainChunks{gat, c->k}, c->P, c->k, c->d, out, nullptr, w, lr));
     }
   } else {
     // HiTopKComm (Alg. 2).  The compressed segment goes straight into this GPU's slot (its node
@@ -576,13 +581,21 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
     // Step 3: inter-node all-gather among the m GPUs at the same position j (Eq. 6), in place ...
     if (c->m > 1) TK_NCCL(c, ncclAllGather(mine, gat, 2 * c->k, ncclUint32, c->col, c->stream));
     mark(c, TK_STAGE_ALLGATHER);
-    float* my_seg = out + (size_t)c->row_pos * c->L;
+    if (c->cfg.step4 == TK_STEP4_DENSE && !out) {  // the dense step 4 gathers the aggregate itself
+      if (!c->h_out) TK_TRY(dev_alloc(c, &c->h_out, c->d));
+      out = c->h_out;
+    }
+    float* my_seg = out ? out + (size_t)c->row_pos * c->L : nullptr;
     if (c->cfg.step4 == TK_STEP4_DENSE) {
       // ... accumulated in group order into this GPU's segment, then step 4: dense intra-node
       // all-gather of the segments (Alg. 2 l.21-23), in place.
       TK_TRY(decompress_impl(c, PlainChunks{gat, c->k}, c->m, c->k, c->L, my_seg));
       TK_NCCL(c, ncclAllGather(my_seg, out, c->L, ncclFloat32, c->row, c->stream));
       mark(c, TK_STAGE_STEP4_ALLGATHER);
+      if (w) {
+        k_sgd_update<<<c->sms * 4, THREADS, 0, c->stream>>>(w, out, c->d, lr);
+        TK_TRY(check_launch(c, "k_sgd_update"));
+      }
     } else {
       // step 4 sparse (Eq. 10): all-gather the m*k~ gathered pairs of every segment, then every
       // GPU accumulates all segments itself (same per-element order -> identical bits).
@@ -590,11 +603,25 @@ tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gat
       mark(c, TK_STAGE_STEP4_ALLGATHER);
       for (uint32_t j = 0; j < c->n; ++j)
         TK_TRY(decompress_impl(c, PlainChunks{c->recv_row + (size_t)j * c->m * 2 * c->k, c->k}, c->m, c->k, c->L,
-                               out + (size_t)j * c->L));
+                               out ? out + (size_t)j * c->L : nullptr, nullptr, w ? w + (size_t)j * c->L : nullptr,
+                               lr));
     }
   }
   c->step++;
   return TK_OK;
+}
+
+tk_status tk_step(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gathered) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (!out) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  return step_impl(c, g, r, out, gathered, nullptr, 0.0f);
+}
+
+tk_status tk_step_sgd(tk_ctx* c, const float* g, float* r, float* w, float lr, float* out, uint32_t* gathered) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (!w) return fail(c, TK_ERR_INVALID_ARG, "null w");
+  if (!(lr == lr) || lr == INFINITY || lr == -INFINITY) return fail(c, TK_ERR_INVALID_ARG, "lr must be finite");
+  return step_impl(c, g, r, out, gathered, w, lr);
 }
 
 tk_status tk_step_host(tk_ctx* c, const float* g_host, uint32_t* gathered_host, float* out_host) {

@@ -1715,10 +1715,14 @@ __device__ uint32_t warp_lower_bound(const Src& src, uint32_t p, uint32_t n, uin
 
 // plain_out (optional): the consumed pairs re-emitted in the plain [nchunks][idx k | val k]
 // layout (each pair lies in exactly one tile, so each is written exactly once)
+// w (optional): the SGD update of Eq. 1 fused into the tile write-back,
+// w_i := fl32(w_i - fl32(lr * out_i)) for every i (two RN operations, no FMA; reading Q29);
+// out (optional when w is given) still receives the aggregate.
 template <class Src>
 __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t nchunks, uint64_t k, uint64_t n,
                                                         uint32_t ntiles, uint32_t tiles_per_cta,
-                                                        float* __restrict__ out, uint32_t* __restrict__ plain_out) {
+                                                        float* __restrict__ out, uint32_t* __restrict__ plain_out,
+                                                        float* __restrict__ w, float lr) {
   __shared__ __align__(16) float s_tile[TILE];
   extern __shared__ uint32_t s_cur[];  // [nchunks] per-rank cursors
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1785,14 +1789,50 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
       __syncthreads();
     }
     if ((uint64_t)thi <= n) {
-      float4* o4 = reinterpret_cast<float4*>(out + tlo);
-      for (int q = threadIdx.x; q < TILE / 4; q += THREADS) __stcs(o4 + q, s4[q]);
+      if (out) {
+        float4* o4 = reinterpret_cast<float4*>(out + tlo);
+        for (int q = threadIdx.x; q < TILE / 4; q += THREADS) __stcs(o4 + q, s4[q]);
+      }
+      if (w) {
+        float4* w4 = reinterpret_cast<float4*>(w + tlo);
+        for (int q = threadIdx.x; q < TILE / 4; q += THREADS) {
+          const float4 v = s4[q];
+          float4 x = __ldcs(w4 + q);
+          x.x = __fsub_rn(x.x, __fmul_rn(lr, v.x));
+          x.y = __fsub_rn(x.y, __fmul_rn(lr, v.y));
+          x.z = __fsub_rn(x.z, __fmul_rn(lr, v.z));
+          x.w = __fsub_rn(x.w, __fmul_rn(lr, v.w));
+          __stcs(w4 + q, x);
+        }
+      }
     } else {
       for (int q = threadIdx.x; q < TILE; q += THREADS)
-        if ((uint64_t)tlo + q < n) out[tlo + q] = s_tile[q];
+        if ((uint64_t)tlo + q < n) {
+          if (out) out[tlo + q] = s_tile[q];
+          if (w) w[tlo + q] = __fsub_rn(w[tlo + q], __fmul_rn(lr, s_tile[q]));
+        }
     }
     __syncthreads();  // s_tile is rewritten by the next tile
   }
+}
+
+// The SGD update of Eq. 1 on a dense aggregate (HiTopKComm dense step 4, where the aggregate is
+// only complete after the row all-gather): w_i := fl32(w_i - fl32(lr * out_i)).
+__global__ void __launch_bounds__(THREADS) k_sgd_update(float* __restrict__ w, const float* __restrict__ out,
+                                                        uint64_t n, float lr) {
+  const uint64_t n4 = n / 4;
+  const uint64_t stride = (uint64_t)gridDim.x * THREADS;
+  for (uint64_t q = (uint64_t)blockIdx.x * THREADS + threadIdx.x; q < n4; q += stride) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(out) + q);
+    float4 x = __ldcs(reinterpret_cast<const float4*>(w) + q);
+    x.x = __fsub_rn(x.x, __fmul_rn(lr, v.x));
+    x.y = __fsub_rn(x.y, __fmul_rn(lr, v.y));
+    x.z = __fsub_rn(x.z, __fmul_rn(lr, v.z));
+    x.w = __fsub_rn(x.w, __fmul_rn(lr, v.w));
+    __stcs(reinterpret_cast<float4*>(w) + q, x);
+  }
+  for (uint64_t i = n4 * 4 + (uint64_t)blockIdx.x * THREADS + threadIdx.x; i < n; i += stride)
+    w[i] = __fsub_rn(w[i], __fmul_rn(lr, out[i]));
 }
 
 // Debug (TK_CHECK=1): a selection / gathered chunk must hold strictly ascending indices < n.

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--rs-mode", default="ordered")
     ap.add_argument("--ag-mode", default="push")
     ap.add_argument("--select", default="mstopk")
+    ap.add_argument("--sgd", type=float, default=0.0, help="also run Eq. 1's fused update with this lr")
     ap.add_argument("--zero-copy", action="store_true", help="write g into the context's input buffer")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
@@ -58,18 +59,26 @@ def main():
     ok = True
     r_ref = [np.zeros(L, np.float32) for _ in range(ws)]
     inbuf = ctx.input_buffer() if a.zero_copy else None
+    w_ref = gradgen.gradient(a.dim, "G", cfg=41)
+    wd = torch.from_numpy(w_ref.copy()).cuda()
     for step in range(a.steps):
         g = torch.from_numpy(gradgen.gradient(a.dim, a.dist, cfg=40, rank=rank, step=step)).cuda()
         if inbuf is not None:
             inbuf.copy_(g)
             g = inbuf
         gat = torch.empty(chunks * 2 * k, dtype=torch.int32, device="cuda")
-        out = ctx.step(g, r, gathered=gat)
+        if a.sgd:
+            out = torch.empty(a.dim, dtype=torch.float32, device="cuda")
+            ctx.step_sgd(g, r, wd, a.sgd, out=out, gathered=gat)
+        else:
+            out = ctx.step(g, r, gathered=gat)
         torch.cuda.synchronize()
         log("step", step, "done")
         outs = [torch.empty_like(out) for _ in range(ws)]
         gats = [torch.empty_like(gat) for _ in range(ws)]
         rs = [torch.empty_like(r) for _ in range(ws)]
+        wds = [torch.empty_like(wd) for _ in range(ws)]
+        dist.all_gather(wds, wd)
         dist.all_gather(outs, out)
         dist.all_gather(gats, gat)
         dist.all_gather(rs, r)
@@ -91,6 +100,11 @@ def main():
             rec["residual_equal"] = [bool(np.array_equal(rr.cpu().numpy().view(np.uint32),
                                                          ref.per_rank[p].residual.view(np.uint32)))
                                      for p, rr in enumerate(rs)]
+            if a.sgd:
+                w_ref = oracle.sgd_update(w_ref, ref.out, a.sgd)
+                rec["w_equal"] = [bool(np.array_equal(x.cpu().numpy().view(np.uint32), w_ref.view(np.uint32)))
+                                  for x in wds]
+                ok = ok and all(rec["w_equal"])
             rec["max_abs_diff"] = max(float(np.max(np.abs(o.cpu().numpy() - ref.out))) for o in outs)
             rec["nnz_out"] = int(np.count_nonzero(ref.out))
             ok = ok and all(rec["out_equal"]) and all(rec["gathered_equal"]) and all(rec["residual_equal"])

@@ -88,3 +88,9 @@ def test_hitopk_c4_full_size(P, n, tmp_path):
 def test_exact_selector_multi_gpu(P, n, tmp_path):
     """the exact top-k selector (Eq. 2) on the flat push path and HiTopKComm"""
     _run(P, tmp_path, dim=8 * 131_076, rho=0.001, group_size=n, select="exact", steps=3)
+
+
+@pytest.mark.parametrize("P,n,step4", [(2, 1, "dense"), (4, 2, "dense"), (4, 2, "sparse")])
+def test_fused_sgd_update_multi_gpu(P, n, step4, tmp_path):
+    """Eq. 1's update fused into the decompression (flat), or after the row all-gather (dense step 4)"""
+    _run(P, tmp_path, dim=8 * 131_076, rho=0.001, group_size=n, step4=step4, sgd=0.05, steps=3)

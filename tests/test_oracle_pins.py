@@ -414,3 +414,20 @@ def test_hitopk_sparsity_bound_and_containment():
         for i in range(m):
             allowed |= set((h.per_rank[i * n + j].sel.idx.astype(np.int64) + j * L).tolist())
         assert set(np.nonzero(h.out[j * L:(j + 1) * L])[0] + j * L) <= allowed
+
+
+# ---------------------------------------------------------------- Eq. 1 update (F4)
+def test_sgd_update_closed_forms_and_exact_rounding():
+    w = gradgen.gradient(4096, "G", cfg=21)
+    g = gradgen.gradient(4096, "H", cfg=22)
+    assert np.array_equal(oracle.sgd_update(w, g, 0.0).view(np.uint32), (w + np.float32(0)).view(np.uint32))
+    assert np.array_equal(oracle.sgd_update(w, np.zeros_like(w), 0.1), w)
+    assert not np.any(oracle.sgd_update(w, w, 1.0))                     # w - w = +0
+    assert not np.any(np.signbit(oracle.sgd_update(w, w, 1.0)))
+    # independent formulation: the fp32 product is the fp64 product (exact for two fp32 operands)
+    # rounded once; the difference of two fp32 values of these magnitudes is exact in fp64, so
+    # rounding it once to fp32 is the correctly rounded fp32 difference
+    lr = np.float32(0.0375)
+    prod = (np.float64(lr) * g.astype(np.float64)).astype(np.float32)
+    want = (w.astype(np.float64) - prod.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(oracle.sgd_update(w, g, float(lr)).view(np.uint32), want.view(np.uint32))
