@@ -55,6 +55,8 @@ def parse():
                     help="HiTopKComm step-1 reduce-scatter: ordered peer reads (bit-exact) or NCCL")
     ap.add_argument("--select", default="mstopk", choices=["mstopk", "exact"],
                     help="selector: MSTopK (Alg. 1) or the exact top-k of Eq. 2 (SURVEY F1)")
+    ap.add_argument("--wire", default="f32", choices=["f32", "f16"],
+                    help="value format on the wire: fp32 or binary16 (SURVEY F3, Fig. 7's FP16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no soak, no e2e, no cpu baseline")
@@ -182,26 +184,26 @@ def sum_over_ranks(x, ws):
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle
-def time_oracle_step(d, rho, N, P, n, seed=1, dist="G", selector="mstopk"):
+def time_oracle_step(d, rho, N, P, n, seed=1, dist="G", selector="mstopk", wire="f32"):
     """One full simulated step of the oracle (all P ranks in one process); returns seconds."""
     import oracle
     gs = [gradgen.gradient(d, dist, cfg=2, rank=p, step=0) for p in range(P)]
     t0 = time.perf_counter()
     if n == 1:
         rs = [np.zeros(d, np.float32) for _ in range(P)]
-        oracle.flat_step(gs, rs, rho, N, seed=seed, selector=selector)
+        oracle.flat_step(gs, rs, rho, N, seed=seed, selector=selector, wire=wire)
     else:
         rs = [np.zeros(d // n, np.float32) for _ in range(P)]
-        oracle.hitopk_step(gs, rs, P // n, n, rho, N, seed=seed, selector=selector)
+        oracle.hitopk_step(gs, rs, P // n, n, rho, N, seed=seed, selector=selector, wire=wire)
     return time.perf_counter() - t0
 
 
 def cpu_baseline(a, P, budget_s=15.0):
     d_s = a.d
-    t = time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist, selector=a.select)
+    t = time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist, selector=a.select, wire=a.wire)
     reps, total = 1, t
     while total < budget_s and reps < 30:
-        total += time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist, selector=a.select)
+        total += time_oracle_step(d_s, a.rho, a.n_iters, 1, 1, dist=a.dist, selector=a.select, wire=a.wire)
         reps += 1
     return {"value": d_s * reps / total, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{reps} full single-rank oracle steps (numpy, 1 thread) at d={d_s}, rho={a.rho}, N={a.n_iters}, "
@@ -215,8 +217,8 @@ def run_reference(a, ws, rank, emit):
     n = a.group_size
     d_s = max(n * 4096, (min(a.d, 25_600_000 // P) // n) * n)  # bounded sample of the workload per step
     for _ in range(a.warmup):
-        time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist, selector=a.select)
-    ts = [time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist, selector=a.select) for _ in range(a.steps)]
+        time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist, selector=a.select, wire=a.wire)
+    ts = [time_oracle_step(d_s, a.rho, a.n_iters, P, n, dist=a.dist, selector=a.select, wire=a.wire) for _ in range(a.steps)]
     t = sum(ts) / len(ts)
     val = P * d_s / t
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
@@ -276,7 +278,7 @@ def main():
     stream = torch.cuda.Stream()
     ctx = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, nranks=P, rank=rank, group_size=n, seed=2010_10458,
                      step4=a.step4, levels_per_pass=a.levels, uid=uid, stream=stream, device=local, ag_mode=a.ag_mode,
-                     select=a.select, rs_mode=a.rs_mode)
+                     select=a.select, rs_mode=a.rs_mode, wire=a.wire)
     L, k = ctx.seg_len, ctx.k
     log("ctx up")
     # inputs: a fresh seeded N(0,1) gradient for every warm-up / timed / profiled step, generated on
@@ -384,7 +386,7 @@ def main():
     if not a.no_e2e and not a.ncu:
         ctx_h = ctx
         hg = [torch.from_numpy(gradgen.gradient(a.d, a.dist, cfg=2, rank=rank, step=s)).pin_memory() for s in range(2)]
-        gat_h = torch.empty(chunks * 2 * k, dtype=torch.int32).pin_memory()
+        gat_h = torch.empty(chunks * ctx.chunk_words, dtype=torch.int32).pin_memory()
         for i in range(3):
             ctx_h.step_host(hg[i % 2], gat_h)
         barrier(ws)
@@ -395,7 +397,7 @@ def main():
         t_e2e = max_over_ranks((time.perf_counter() - t0) / ks, ws)
         log("e2e done")
         e2e = {"value": P * a.d / t_e2e, "unit": UNIT, "ms_per_step": t_e2e * 1e3,
-               "h2d_bytes_per_step": 4 * a.d, "d2h_bytes_per_step": 4 * chunks * 2 * k,
+               "h2d_bytes_per_step": 4 * a.d, "d2h_bytes_per_step": 4 * chunks * ctx.chunk_words,
                "api": "tk_step_host (pinned host gradient in, gathered (index, value) pairs out; residual device-resident)"}
 
     cpu = None
@@ -409,6 +411,7 @@ def main():
                 "config": {"workload": workload_name(a, P), "d": a.d, "rho": a.rho, "k": k, "n_iters": a.n_iters,
                            "P": P, "group_size": n, "step4": a.step4 if n > 1 else None, "dist": a.dist,
                            "allgather": (a.ag_mode if n == 1 and P > 1 else None), "selector": a.select,
+                           "wire": a.wire,
                            "levels_per_pass": a.levels or 10, "input_buffers": nbuf,
                            "inputs": "fresh seeded N(0,1) gradient per step (torch CUDA generator, pre-generated in "
                                      "HBM); residual carried from r=0 at step 0; timed steps W..W+K-1",

@@ -63,6 +63,13 @@ enum { TK_SELECT_MSTOPK = 0, TK_SELECT_EXACT = 1 }; /* selector:
                                                      EXACT = exact top-k of Eq. 2:
                                                      the k largest |acc|, ties -> lower index (Q6);
                                                      n_iters is then unused                     */
+enum { TK_WIRE_F32 = 0, TK_WIRE_F16 = 1 };         /* value format on the wire (Fig. 7
+                                                     ran FP16; reading Q31): F16 = each
+                                                     selected value v is sent as
+                                                     fp16_RN(clamp(v, +-65504)) and the residual
+                                                     keeps fl32(v - sent) instead of +0; a packed
+                                                     chunk is then [idx k | binary16 val k] padded
+                                                     to k + ceil(k/2) u32 words (6k bytes + pad)  */
 enum { TK_RS_ORDERED = 0, TK_RS_NCCL = 1 };       /* HiTopKComm step 1 reduce-scatter (Q20):
                                                      ORDERED = ascending-row-rank fp32 sum read over
                                                      NVLink peer pointers inside the EF kernel
@@ -90,6 +97,7 @@ typedef struct tk_config {
   uint32_t rs_mode;        /* HiTopKComm step-1 mode (TK_RS_ORDERED or TK_RS_NCCL)             */
   uint32_t ag_mode;        /* flat all-gather mode (TK_AG_PUSH or TK_AG_NCCL)                  */
   uint32_t select;         /* TK_SELECT_MSTOPK (default) or TK_SELECT_EXACT                    */
+  uint32_t wire;           /* TK_WIRE_F32 (default) or TK_WIRE_F16 (values sent as binary16)  */
 } tk_config;
 
 /* Snapshot of the last compression's MSTopK control block (for parity checks). */
@@ -138,16 +146,18 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
  *   g   [d]  in     gradient (never written)
  *   r   [d]  in/out residual r -> r' (error_feedback = 1); ignored when error_feedback = 0
  *   idx [k]  out    selected indices iota, strictly ascending (Q11)
- *   val [k]  out    kappa = acc[iota], bit-copied (Q12)
+ *   val [k]  out    kappa = acc[iota], bit-copied (Q12); TK_WIRE_F16: the fp16-rounded values sent
  * g must not alias r, idx or val. */
 tk_status tk_compress(tk_ctx* ctx, const float* g, float* r, uint32_t* idx, float* val);
 
-/* Sparse All-Gather: gathered [P][2k] u32, rank-major, each rank's chunk laid out as
- * [idx k | bits(val) k] (Q15).  idx/val are this rank's tk_compress outputs.  Collective. */
+/* Sparse All-Gather: gathered [P][cw] u32, rank-major, each rank's chunk laid out as
+ * [idx k | bits(val) k] (Q15, cw = 2k) or, with TK_WIRE_F16, [idx k | binary16 val k] padded to
+ * cw = k + ceil(k/2) words.  idx/val are this rank's tk_compress outputs (with TK_WIRE_F16 the
+ * values are already the fp16-rounded ones).  Collective. */
 tk_status tk_sparse_allgather(tk_ctx* ctx, const uint32_t* idx, const float* val, uint32_t* gathered);
 
 /* Rank-ordered index accumulation (Alg. 2 l.15-20): out = +0^d; for p = 0..nchunks-1 in order:
- * out[idx_p] += val_p in fp32 round-to-nearest (Q16).  gathered is [nchunks][2k] as above, each
+ * out[idx_p] += val_p in fp32 round-to-nearest (Q16).  gathered is [nchunks][cw] as above, each
  * chunk's indices strictly ascending and < d (violations: memory-safe, result unspecified).
  * nchunks in [1, 4096]; out has d elements (flat) or d/n (HiTopKComm segment).  A larger
  * nchunks than any previous call grows an internal table (synchronises the stream). */
@@ -157,7 +167,7 @@ tk_status tk_decompress(tk_ctx* ctx, const uint32_t* gathered, uint32_t nchunks,
  *   g   [d]            in      local gradient
  *   r   [d] or [d/n]   in/out  residual (flat: d; HiTopKComm: the segment length d/n, Q22)
  *   out [d]            out     aggregated sparse gradient, bitwise identical on every rank
- *   gathered           out     optional (NULL = internal): flat [P][2k]; HiTopKComm [m][2k~]
+ *   gathered           out     optional (NULL = internal): flat [P][cw]; HiTopKComm [m][cw~]
  * Increments the step counter after enqueueing. */
 tk_status tk_step(tk_ctx* ctx, const float* g, float* r, float* out, uint32_t* gathered);
 

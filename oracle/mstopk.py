@@ -206,11 +206,12 @@ class CompressResult:
     sel: MSTopKResult
     acc: np.ndarray        # the vector MSTopK ran on (g + r with error feedback, else g)
     residual: np.ndarray   # r' (error feedback) — None when EF is off
+    sent: np.ndarray       # the values put on the wire: sel.val, or their binary16 rounding (F3)
 
 
 def compress(g: np.ndarray, r: np.ndarray | None, k: int, n_iters: int, *, seed: int = 0,
              step: int = 0, rank: int = 0, rand_mode: int = RAND_SEEDED,
-             error_feedback: bool = True, selector: str = "mstopk") -> CompressResult:
+             error_feedback: bool = True, selector: str = "mstopk", wire: str = "f32") -> CompressResult:
     """One rank's compression with error feedback (BJ north_star; Q14):
     acc = fl32(g + r); (kappa, iota) = MSTopK(acc) -- or, with selector="exact", the exact top-k
     of Eq. 2 (TopK-SGD; ties -> lower index, Q6); r' = acc with the sent entries := +0.0."""
@@ -225,8 +226,18 @@ def compress(g: np.ndarray, r: np.ndarray | None, k: int, n_iters: int, *, seed:
         sel = mstopk(acc, k, n_iters, seed=seed, step=step, rank=rank, rand_mode=rand_mode)
     else:
         raise ValueError(f"unknown selector {selector!r}")
+    if wire == "f32":
+        sent = sel.val.copy()
+    elif wire == "f16":
+        # FP16 wire values (F3; Fig. 7 ran FP16; reading Q31): round-to-nearest binary16 of
+        # the value clamped to the finite range, widened back exactly
+        sent = np.clip(sel.val, np.float32(-65504.0), np.float32(65504.0)).astype(np.float16).astype(np.float32)
+    else:
+        raise ValueError(f"unknown wire format {wire!r}")
     res = None
     if error_feedback:
         res = acc.copy()
-        res[sel.idx.astype(np.int64)] = np.float32(0.0)
-    return CompressResult(sel=sel, acc=acc, residual=res)
+        ii = sel.idx.astype(np.int64)
+        # Q14: the sent entries keep what was not sent: +0 (fp32 wire), fl32(v - sent) (FP16 wire)
+        res[ii] = np.float32(0.0) if wire == "f32" else (sel.val - sent).astype(np.float32)
+    return CompressResult(sel=sel, acc=acc, residual=res, sent=sent)

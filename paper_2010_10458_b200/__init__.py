@@ -39,7 +39,7 @@ class _Config(ctypes.Structure):
                 ("group_size", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("rand_mode", ctypes.c_uint32),
                 ("error_feedback", ctypes.c_uint32), ("step4", ctypes.c_uint32),
                 ("levels_per_pass", ctypes.c_uint32), ("device", ctypes.c_int32), ("rs_mode", ctypes.c_uint32),
-                ("ag_mode", ctypes.c_uint32), ("select", ctypes.c_uint32)]
+                ("ag_mode", ctypes.c_uint32), ("select", ctypes.c_uint32), ("wire", ctypes.c_uint32)]
 
 
 class _Stats(ctypes.Structure):
@@ -195,13 +195,14 @@ class _DeviceView:
 class Context:
     """One rank's libtk context (tk_init).  ``d, rho, n_iters`` follow the paper's statement of
     the problem (x in R^d, k = rho*d, N samplings, P workers, m x n for HiTopKComm).
-    ``select="exact"`` replaces MSTopK by the exact top-k of Eq. 2 (ties -> lower index)."""
+    ``select="exact"`` replaces MSTopK by the exact top-k of Eq. 2 (ties -> lower index);
+    ``wire="f16"`` sends the values as binary16 (Fig. 7's FP16, reading Q31)."""
 
     def __init__(self, d: int, rho: float = 0.001, n_iters: int = 10, *, k: int = 0, nranks: int = 1, rank: int = 0,
                  group_size: int = 1, seed: int = 0, rand_mode: str = "seeded", error_feedback: bool = True,
                  step4: str = "dense", levels_per_pass: int = 0, device: int | None = None, uid: bytes | None = None,
                  stream: torch.cuda.Stream | None = None, rs_mode: str = "ordered", ag_mode: str = "push",
-                 select: str = "mstopk"):
+                 select: str = "mstopk", wire: str = "f32"):
         if not torch.cuda.is_available():
             raise RuntimeError("libtk needs a CUDA device (B200, sm_100a); there is no CPU fallback")
         dev = torch.cuda.current_device() if device is None else int(device)
@@ -212,7 +213,7 @@ class Context:
                       rand_mode={"seeded": 0, "first": 1}[rand_mode], error_feedback=1 if error_feedback else 0,
                       step4={"dense": 0, "sparse": 1}[step4], levels_per_pass=int(levels_per_pass), device=dev,
                       rs_mode={"ordered": 0, "nccl": 1}[rs_mode], ag_mode={"push": 0, "nccl": 1}[ag_mode],
-                      select={"mstopk": 0, "exact": 1}[select])
+                      select={"mstopk": 0, "exact": 1}[select], wire={"f32": 0, "f16": 1}[wire])
         self._ctx = ctypes.c_void_p()
         if nranks > 1 and uid is None:
             raise ValueError("nranks > 1 needs the NCCL unique id (broadcast_unique_id())")
@@ -225,6 +226,9 @@ class Context:
         self.d, self.k, self.seg_len = int(d), k_.value, L.value
         self.nranks, self.m, self.n, self.rank = P.value, m.value, n.value, int(rank)
         self.error_feedback = bool(error_feedback)
+        self.wire = wire
+        # u32 words of one packed chunk: [idx k | fp32 val k] or [idx k | binary16 val k (padded)]
+        self.chunk_words = 2 * self.k if wire == "f32" else self.k + (self.k + 1) // 2
 
     # -------------------------------------------------------------------------------------
     def _check(self, st):
@@ -248,7 +252,7 @@ class Context:
         return idx, val
 
     def sparse_allgather(self, idx, val, gathered=None):
-        gathered = self._empty(self.chunks * 2 * self.k, torch.int32) if gathered is None else gathered
+        gathered = self._empty(self.chunks * self.chunk_words, torch.int32) if gathered is None else gathered
         self._check(_lib.tk_sparse_allgather(self._ctx, _ptr(idx, "idx", torch.int32), _ptr(val, "val", torch.float32),
                                              _ptr(gathered, "gathered", torch.int32)))
         return gathered

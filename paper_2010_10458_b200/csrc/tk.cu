@@ -31,6 +31,7 @@ struct tk_ctx {
   uint32_t P = 1, m = 1, n = 1, rank = 0;
   uint32_t row_pos = 0, col_pos = 0;  // j = rank % n (position in the node), i = rank / n (node)
   uint64_t d = 0, L = 0, k = 0;       // L = d / n (segment length); k = k (flat) or k~ (HiTopK)
+  uint64_t cw = 0;                    // u32 words per packed chunk: 2k (fp32 values) or k + ceil(k/2) (FP16 wire)
   uint32_t sms = 148;
   uint32_t grid = 0;                  // CTAs of the cooperative compression kernel
   uint32_t W = 0;                     // warp slabs
@@ -161,7 +162,7 @@ int peer_sources(const tk_ctx* c) { return (c->n > 1 && c->cfg.rs_mode == TK_RS_
 // cooperative launch of k_compress.  With peers != nullptr the gradient is the ordered sum of the
 // np peer segments (HiTopKComm step 1).
 tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, float* val, const Peers* peers = nullptr,
-                        int np = 0, const PushOut* push = nullptr) {
+                        int np = 0, const PushOut* push = nullptr, uint16_t* val16 = nullptr) {
   const bool ef = c->cfg.error_feedback != 0;
   Fused f;
   memset(&f, 0, sizeof(f));
@@ -181,6 +182,8 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.cp = c->cp;
   f.idx_out = idx;
   f.val_out = val;
+  f.val16_out = val16;
+  f.wire16 = c->cfg.wire == TK_WIRE_F16 ? 1u : 0u;
   if (push) f.push = *push;
   f.c = c->ctrl;
   f.step = c->step;
@@ -214,16 +217,35 @@ tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t 
   const uint32_t per = (nt + max_cta - 1) / max_cta;
   const uint32_t grid = (nt + per - 1) / per;
   if (c->debug_check) {
-    if constexpr (std::is_same<Src, PlainChunks>::value)
+    if constexpr (std::is_same<Src, PlainChunks>::value || std::is_same<Src, PlainChunks16>::value)
       for (uint32_t p = 0; p < nchunks; ++p)
-        k_check_sel<<<1, 1024, 0, c->stream>>>(src.g + (size_t)p * 2 * kk, kk, len, (uint32_t)c->rank, (uint32_t)c->step,
+        k_check_sel<<<1, 1024, 0, c->stream>>>(src.g + (size_t)p * c->cw, kk, len, (uint32_t)c->rank, (uint32_t)c->step,
                                                1u + p);
   }
   k_decompress<Src><<<grid, THREADS, sizeof(uint32_t) * nchunks, c->stream>>>(src, nchunks, kk, len, nt, per, out,
-                                                                               plain_out, w, lr);
+                                                                               plain_out, w, lr, c->cw,
+                                                                               c->cfg.wire == TK_WIRE_F16 ? 1u : 0u);
   TK_TRY(check_launch(c, "k_decompress"));
   mark(c, TK_STAGE_DECOMPRESS);
   return TK_OK;
+}
+
+// decompression of packed chunks in the context's wire format
+tk_status decompress_plain(tk_ctx* c, const uint32_t* base, uint32_t nchunks, uint64_t len, float* out,
+                           float* w = nullptr, float lr = 0.0f) {
+  if (c->cfg.wire == TK_WIRE_F16)
+    return decompress_impl(c, PlainChunks16{base, c->k, c->cw}, nchunks, c->k, len, out, nullptr, w, lr);
+  return decompress_impl(c, PlainChunks{base, c->k}, nchunks, c->k, len, out, nullptr, w, lr);
+}
+
+// where the selection writes its values inside a packed chunk
+struct ChunkOut {
+  float* val;
+  uint16_t* val16;
+};
+ChunkOut chunk_out(const tk_ctx* c, uint32_t* chunk) {
+  if (c->cfg.wire == TK_WIRE_F16) return {nullptr, reinterpret_cast<uint16_t*>(chunk + c->k)};
+  return {reinterpret_cast<float*>(chunk + c->k), nullptr};
 }
 
 template <typename T>
@@ -376,7 +398,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if (k.n_iters < 1 || k.n_iters > (uint32_t)NMAX) return TK_ERR_INVALID_ARG;
   if (k.nranks < 1 || k.rank >= k.nranks) return TK_ERR_INVALID_ARG;
   if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 10 || k.rs_mode > 1 ||
-      k.ag_mode > 1 || k.select > 1)
+      k.ag_mode > 1 || k.select > 1 || k.wire > 1)
     return TK_ERR_INVALID_ARG;
   const uint32_t n = k.group_size == 0 ? 1 : k.group_size;
   if (k.nranks % n != 0) return TK_ERR_CONFIG;
@@ -437,13 +459,14 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if ((s = plan_launches(c)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->wcnt, (size_t)c->npass * TMAX * c->W)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->ctrl, 1)) != TK_OK) return bail(s);
-  if ((s = dev_alloc(c, &c->send, 2 * kk)) != TK_OK) return bail(s);
+  c->cw = (k.wire == TK_WIRE_F16) ? kk + (kk + 1) / 2 : 2 * kk;
+  if ((s = dev_alloc(c, &c->send, c->cw)) != TK_OK) return bail(s);
   const uint32_t chunks_recv = (n == 1) ? c->P : c->m;
-  if ((s = dev_alloc(c, &c->recv, (size_t)chunks_recv * 2 * kk)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->recv, (size_t)chunks_recv * c->cw)) != TK_OK) return bail(s);
   if (n > 1) {
     if (k.rs_mode == TK_RS_NCCL && (s = dev_alloc(c, &c->seg, L)) != TK_OK) return bail(s);
     if (k.step4 == TK_STEP4_SPARSE)
-      if ((s = dev_alloc(c, &c->recv_row, (size_t)n * c->m * 2 * kk)) != TK_OK) return bail(s);
+      if ((s = dev_alloc(c, &c->recv_row, (size_t)n * c->m * c->cw)) != TK_OK) return bail(s);
   }
   if (cudaMemset(c->ctrl, 0, sizeof(Ctrl)) != cudaSuccess) return bail(TK_ERR_CUDA);
   if (c->P > 1) {
@@ -482,19 +505,24 @@ tk_status tk_sparse_allgather(tk_ctx* c, const uint32_t* idx, const float* val, 
   if (!idx || !val || !gathered) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
   const size_t kb = sizeof(uint32_t) * c->k;
   const uint32_t* src = c->send;
-  if ((const void*)val == (const void*)(idx + c->k)) {
+  if (c->cfg.wire == TK_WIRE_F16) {
+    // FP16 wire: pack [idx | binary16 val] (the values tk_compress returned are already fp16-exact)
+    k_pack16<<<(unsigned)((c->k + THREADS - 1) / THREADS), THREADS, 0, c->stream>>>(idx, val, c->send, c->k);
+    TK_TRY(check_launch(c, "k_pack16"));
+  } else if ((const void*)val == (const void*)(idx + c->k)) {
     src = idx;  // caller already holds the packed [idx | val] layout
   } else {
     TK_CUDA(c, cudaMemcpyAsync(c->send, idx, kb, cudaMemcpyDeviceToDevice, c->stream));
     TK_CUDA(c, cudaMemcpyAsync(c->send + c->k, val, kb, cudaMemcpyDeviceToDevice, c->stream));
   }
   if (c->P == 1) {
-    if (src != gathered) TK_CUDA(c, cudaMemcpyAsync(gathered, src, 2 * kb, cudaMemcpyDeviceToDevice, c->stream));
+    if (src != gathered)
+      TK_CUDA(c, cudaMemcpyAsync(gathered, src, sizeof(uint32_t) * c->cw, cudaMemcpyDeviceToDevice, c->stream));
     return TK_OK;
   }
   ncclComm_t comm = (c->n == 1) ? c->world : c->col;
   if (!comm) return fail(c, TK_ERR_STATE, "no communicator for the sparse all-gather");
-  TK_NCCL(c, ncclAllGather(src, gathered, 2 * c->k, ncclUint32, comm, c->stream));
+  TK_NCCL(c, ncclAllGather(src, gathered, c->cw, ncclUint32, comm, c->stream));
   return TK_OK;
 }
 
@@ -504,7 +532,7 @@ tk_status tk_decompress(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, f
   if (!aligned16(out)) return fail(c, TK_ERR_INVALID_ARG, "out must be 16-byte aligned");
   if (nchunks < 1 || nchunks > 4096) return fail(c, TK_ERR_INVALID_ARG, "nchunks must lie in [1, 4096]");
   const uint64_t len = (c->n == 1) ? c->d : c->L;
-  return decompress_impl(c, PlainChunks{gathered, c->k}, nchunks, c->k, len, out);
+  return decompress_plain(c, gathered, nchunks, len, out);
 }
 
 // One iteration (tk_step / tk_step_sgd).  w != nullptr: Eq. 1's update fused into the final
@@ -524,7 +552,8 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
     // flat NaiveAG: compress straight into this rank's slot of the gathered buffer -> one packed
     // in-place all-gather -> rank-ordered decompress
     uint32_t* gat = gathered ? gathered : c->recv;
-    uint32_t* mine = gat + (size_t)c->rank * 2 * c->k;
+    uint32_t* mine = gat + (size_t)c->rank * c->cw;
+    const ChunkOut co = chunk_out(c, mine);
     if (c->P > 1 && c->pg) {
       // fused all-gather (TK_AG_PUSH): the compression selects into this rank's plain slot, then
       // each CTA pushes its run of pairs as tagged packets into this rank's chunk on every GPU;
@@ -540,22 +569,23 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
       po.me = c->rank;
       po.tag = c->push_seq + 1;
       for (uint32_t q = 0; q < c->P; ++q) po.slot[q] = c->peer_pg[q] + parity * stride + (size_t)c->rank * c->k;
-      TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k), nullptr, 0, &po));
+      TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, co.val, nullptr, 0, &po, co.val16));
       c->push_seq++;
       mark(c, TK_STAGE_ALLGATHER);
       TaggedChunks src{c->pg + parity * stride, c->k, po.tag};
       TK_TRY(decompress_impl(c, src, c->P, c->k, c->d, out, gat, w, lr));
     } else {
-      TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k)));
-      if (c->P > 1) TK_NCCL(c, ncclAllGather(mine, gat, 2 * c->k, ncclUint32, c->world, c->stream));
+      TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, co.val, nullptr, 0, nullptr, co.val16));
+      if (c->P > 1) TK_NCCL(c, ncclAllGather(mine, gat, c->cw, ncclUint32, c->world, c->stream));
       mark(c, TK_STAGE_ALLGATHER);
-      TK_TRY(decompress_impl(c, PlainChunks{gat, c->k}, c->P, c->k, c->d, out, nullptr, w, lr));
+      TK_TRY(decompress_plain(c, gat, c->P, c->d, out, w, lr));
     }
   } else {
     // HiTopKComm (Alg. 2).  The compressed segment goes straight into this GPU's slot (its node
     // index i = col_pos) of the column-gathered buffer.
     uint32_t* gat = gathered ? gathered : c->recv;
-    uint32_t* mine = gat + (size_t)c->col_pos * 2 * c->k;
+    uint32_t* mine = gat + (size_t)c->col_pos * c->cw;
+    const ChunkOut co = chunk_out(c, mine);
     // Step 1: intra-node reduce-scatter of g (Eq. 4) ...
     if (c->cfg.rs_mode == TK_RS_ORDERED) {
       // ... ordered, read by this GPU's EF kernel straight from the row peers' buffers: make g
@@ -570,16 +600,15 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
       memset(&pr, 0, sizeof(pr));
       for (uint32_t q = 0; q < c->n; ++q) pr.p[q] = c->peer_g[q] + (size_t)c->row_pos * c->L;
       // Step 2 (fused with step 1): MSTopK on the segment with k~ (Eq. 5), EF on the segment residual.
-      TK_TRY(compress_impl(c, nullptr, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k), &pr,
-                           (int)c->n));
+      TK_TRY(compress_impl(c, nullptr, ef ? r : nullptr, mine, co.val, &pr, (int)c->n, nullptr, co.val16));
     } else {
       TK_NCCL(c, ncclReduceScatter(g, c->seg, c->L, ncclFloat32, ncclSum, c->row, c->stream));
       mark(c, TK_STAGE_REDUCE_SCATTER);
       // Step 2: MSTopK on the segment with k~ (Eq. 5), error feedback on the segment residual.
-      TK_TRY(compress_impl(c, c->seg, ef ? r : nullptr, mine, reinterpret_cast<float*>(mine + c->k)));
+      TK_TRY(compress_impl(c, c->seg, ef ? r : nullptr, mine, co.val, nullptr, 0, nullptr, co.val16));
     }
     // Step 3: inter-node all-gather among the m GPUs at the same position j (Eq. 6), in place ...
-    if (c->m > 1) TK_NCCL(c, ncclAllGather(mine, gat, 2 * c->k, ncclUint32, c->col, c->stream));
+    if (c->m > 1) TK_NCCL(c, ncclAllGather(mine, gat, c->cw, ncclUint32, c->col, c->stream));
     mark(c, TK_STAGE_ALLGATHER);
     if (c->cfg.step4 == TK_STEP4_DENSE && !out) {  // the dense step 4 gathers the aggregate itself
       if (!c->h_out) TK_TRY(dev_alloc(c, &c->h_out, c->d));
@@ -589,7 +618,7 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
     if (c->cfg.step4 == TK_STEP4_DENSE) {
       // ... accumulated in group order into this GPU's segment, then step 4: dense intra-node
       // all-gather of the segments (Alg. 2 l.21-23), in place.
-      TK_TRY(decompress_impl(c, PlainChunks{gat, c->k}, c->m, c->k, c->L, my_seg));
+      TK_TRY(decompress_plain(c, gat, c->m, c->L, my_seg));
       TK_NCCL(c, ncclAllGather(my_seg, out, c->L, ncclFloat32, c->row, c->stream));
       mark(c, TK_STAGE_STEP4_ALLGATHER);
       if (w) {
@@ -599,12 +628,11 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
     } else {
       // step 4 sparse (Eq. 10): all-gather the m*k~ gathered pairs of every segment, then every
       // GPU accumulates all segments itself (same per-element order -> identical bits).
-      TK_NCCL(c, ncclAllGather(gat, c->recv_row, (size_t)c->m * 2 * c->k, ncclUint32, c->row, c->stream));
+      TK_NCCL(c, ncclAllGather(gat, c->recv_row, (size_t)c->m * c->cw, ncclUint32, c->row, c->stream));
       mark(c, TK_STAGE_STEP4_ALLGATHER);
       for (uint32_t j = 0; j < c->n; ++j)
-        TK_TRY(decompress_impl(c, PlainChunks{c->recv_row + (size_t)j * c->m * 2 * c->k, c->k}, c->m, c->k, c->L,
-                               out ? out + (size_t)j * c->L : nullptr, nullptr, w ? w + (size_t)j * c->L : nullptr,
-                               lr));
+        TK_TRY(decompress_plain(c, c->recv_row + (size_t)j * c->m * c->cw, c->m, c->L,
+                                out ? out + (size_t)j * c->L : nullptr, w ? w + (size_t)j * c->L : nullptr, lr));
     }
   }
   c->step++;
@@ -637,7 +665,7 @@ tk_status tk_step_host(tk_ctx* c, const float* g_host, uint32_t* gathered_host, 
   TK_TRY(tk_step(c, c->h_g, c->h_r, c->h_out, nullptr));
   if (gathered_host) {
     const size_t chunks = (c->n == 1) ? c->P : c->m;
-    TK_CUDA(c, cudaMemcpyAsync(gathered_host, c->recv, sizeof(uint32_t) * chunks * 2 * c->k, cudaMemcpyDeviceToHost,
+    TK_CUDA(c, cudaMemcpyAsync(gathered_host, c->recv, sizeof(uint32_t) * chunks * c->cw, cudaMemcpyDeviceToHost,
                                c->stream));
   }
   if (out_host)

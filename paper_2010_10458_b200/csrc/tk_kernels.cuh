@@ -10,6 +10,7 @@
 // Citations: P:n = PAPER.md line n.  Q<n> = numbered reading in DESIGN.md.
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace tk {
@@ -149,6 +150,16 @@ struct PlainChunks {  // [nchunks][idx k | val k] u32
   __device__ __forceinline__ void get(uint32_t p, uint32_t j, uint32_t& i, float& v) const {
     i = __ldg(g + (size_t)p * 2 * k + j);
     v = __uint_as_float(__ldg(g + (size_t)p * 2 * k + k + j));
+  }
+};
+
+struct PlainChunks16 {  // FP16 wire: [nchunks][idx k | binary16 val k (padded to whole words)] (stride cw words)
+  const uint32_t* g;
+  uint64_t k, cw;
+  __device__ __forceinline__ uint32_t idx(uint32_t p, uint32_t j) const { return __ldg(g + (size_t)p * cw + j); }
+  __device__ __forceinline__ void get(uint32_t p, uint32_t j, uint32_t& i, float& v) const {
+    i = __ldg(g + (size_t)p * cw + j);
+    v = __half2float(__ushort_as_half(__ldg(reinterpret_cast<const unsigned short*>(g + (size_t)p * cw + k) + j)));
   }
 };
 
@@ -1004,10 +1015,32 @@ __device__ __forceinline__ void hist_to_counts(const uint32_t* ghist, int lev, u
 // slab's exclusive prefix counts; rounds without any class-1/2 element cost a ballot only, and a
 // slab that provably holds no kept element is not read at all.
 // HBM/L2: <= 4 B/elem read + 8 B per selected pair + a 4-byte residual zero per selected pair.
+// Where a selected pair goes (A7) and what stays in the residual (A8).  FP16 wire values (F3,
+// reading Q31): the value sent is v16 = fp16_RN(clamp(v, +-65504)); the residual keeps
+// fl32(v - v16) instead of +0.
+struct SelOut {
+  uint32_t* idx;
+  float* val;       // fp32 value sent (optional)
+  uint16_t* val16;  // binary16 value sent (optional; FP16 wire)
+  float* r;         // residual write-back (EF; nullptr without)
+  uint32_t w16;
+};
+
+__device__ __forceinline__ void put_sel(const SelOut& o, uint32_t pos, uint32_t i, float v) {
+  o.idx[pos] = i;
+  float sent = v;
+  if (o.w16) {
+    const __half h = __float2half_rn(fminf(fmaxf(v, -65504.0f), 65504.0f));
+    sent = __half2float(h);
+    if (o.val16) o.val16[pos] = __half_as_ushort(h);
+  }
+  if (o.val) o.val[pos] = sent;
+  if (o.r) o.r[i] = o.w16 ? __fsub_rn(v, sent) : 0.0f;
+}
+
 __device__ __forceinline__ void select_phase(const float* __restrict__ acc, const Ctrl* c, const SearchParams sp,
-                                          uint32_t c1, uint32_t c2, uint32_t b1, uint32_t b2,
-                                          uint32_t* __restrict__ idx_out, float* __restrict__ val_out,
-                                          float* __restrict__ r_zero, const Compact cp) {
+                                          uint32_t c1, uint32_t c2, uint32_t b1, uint32_t b2, const SelOut& so,
+                                          const Compact cp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint64_t lo = min(sp.n, (uint64_t)gw * sp.S);
@@ -1065,15 +1098,13 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
           const uint32_t after = (q2 > rnd) ? min(q2 - rnd, need) : 0u;
           const uint32_t pos = q1 + after;
           TK_DCHECK(pos < sp.k && ii[e] < sp.n, "sel-cap1", pos, ii[e]);
-          { idx_out[pos] = ii[e]; val_out[pos] = __uint_as_float(bb[e]); }
-          if (r_zero) r_zero[ii[e]] = 0.0f;
+          put_sel(so, pos, ii[e], __uint_as_float(bb[e]));
           ++q1;
         } else if (fc2 & (1u << e)) {
           if (q2 >= rnd && q2 < rnd + need) {
             const uint32_t pos = q1 + (q2 - rnd);
             TK_DCHECK(pos < sp.k && ii[e] < sp.n, "sel-cap2", pos, ii[e]);
-            { idx_out[pos] = ii[e]; val_out[pos] = __uint_as_float(bb[e]); }
-            if (r_zero) r_zero[ii[e]] = 0.0f;
+            put_sel(so, pos, ii[e], __uint_as_float(bb[e]));
           }
           ++q2;
         }
@@ -1117,15 +1148,13 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
           const uint32_t after = (q2 > rnd) ? min(q2 - rnd, need) : 0u;
           const uint32_t pos = q1 + after;
           TK_DCHECK(pos < sp.k && i < sp.n, "sel-full1", pos, i);
-          { idx_out[pos] = i; val_out[pos] = __uint_as_float(__ldg(a32 + i)); }
-          if (r_zero) r_zero[i] = 0.0f;
+          put_sel(so, pos, i, __uint_as_float(__ldg(a32 + i)));
           ++q1;
         } else {
           if (q2 >= rnd && q2 < rnd + need) {
             const uint32_t pos = q1 + (q2 - rnd);
             TK_DCHECK(pos < sp.k && i < sp.n, "sel-full2", pos, i);
-            { idx_out[pos] = i; val_out[pos] = __uint_as_float(__ldg(a32 + i)); }
-            if (r_zero) r_zero[i] = 0.0f;
+            put_sel(so, pos, i, __uint_as_float(__ldg(a32 + i)));
           }
           ++q2;
         }
@@ -1209,6 +1238,8 @@ struct Fused {
   int cap_levels;            // max levels per later pass on compacted entries (whole-vector: <= 2)
   int max_pass;              // passes for which totals / wcnt are allocated
   uint32_t ef_compact;       // 1: compact in the ef phase at the key the previous call predicted
+  uint16_t* val16_out;       // FP16 wire: binary16 values of the selection (nullptr: none)
+  uint32_t wire16;           // FP16 wire values (F3): round the values sent, keep the error in r
 };
 
 // Grid-wide barrier (the launch is cooperative: every CTA is resident).  Arrivals are counted
@@ -1288,7 +1319,10 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   stamp();
   for (int i = blockIdx.x * THREADS + tid; i < HIST_BINS * HREP * f.max_pass; i += gridDim.x * THREADS)
     f.totals[i] = 0u;
-  if (blockIdx.x == 0 && tid == 0) { f.flags[0] = 0u; f.flags[1] = 0u; f.flags[2] = 0u; }
+  if (blockIdx.x == 0 && tid == 0) {
+    f.flags[0] = 0u; f.flags[1] = 0u; f.flags[2] = 0u;
+    if (f.val16_out && (f.sp.k & 1u)) f.val16_out[f.sp.k] = 0u;  // FP16 wire: the chunk's padding half
+  }
   // ---- A1-A2: error feedback, |acc| pairwise tree and max; compaction at the key the previous
   // call predicted (its entries replace the whole-vector first count pass when they are exact) ----
   const uint32_t efk = f.ef_compact ? sc.ef_key : 0u;
@@ -1646,7 +1680,15 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   uint32_t b1 = s_base[0], b2 = s_base[1];
   for (int w = 0; w < warp; ++w) { b1 += s_w[0][w]; b2 += s_w[1][w]; }
   // ---- A7-A8: selection, compaction, residual write-back ----
-  select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, f.idx_out, f.val_out, EF ? f.r : nullptr, f.cp);
+  {
+    SelOut so;
+    so.idx = f.idx_out;
+    so.val = f.val_out;
+    so.val16 = f.val16_out;
+    so.r = EF ? f.r : nullptr;
+    so.w16 = f.wire16;
+    select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, so, f.cp);
+  }
   stamp();
   if (f.push.np > 0) {
     // Fused all-gather.  The kept elements of this CTA occupy ONE contiguous run of output
@@ -1662,7 +1704,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     __syncthreads();
     for (uint32_t pos = p0 + tid; pos < p1; pos += THREADS) {
       const uint32_t i = __ldcg(f.idx_out + pos);
-      const uint32_t v = __ldcg(reinterpret_cast<const uint32_t*>(f.val_out) + pos);
+      const uint32_t v = f.val16_out ? __float_as_uint(__half2float(__ushort_as_half(__ldcg(f.val16_out + pos))))
+                                     : __ldcg(reinterpret_cast<const uint32_t*>(f.val_out) + pos);
       for (uint32_t q = 0; q < f.push.np; ++q) st_ll(f.push.slot[q] + pos, i, v, f.push.tag);
     }
   }
@@ -1722,7 +1765,7 @@ template <class Src>
 __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t nchunks, uint64_t k, uint64_t n,
                                                         uint32_t ntiles, uint32_t tiles_per_cta,
                                                         float* __restrict__ out, uint32_t* __restrict__ plain_out,
-                                                        float* __restrict__ w, float lr) {
+                                                        float* __restrict__ w, float lr, uint64_t cw, uint32_t w16) {
   __shared__ __align__(16) float s_tile[TILE];
   extern __shared__ uint32_t s_cur[];  // [nchunks] per-rank cursors
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1731,8 +1774,14 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
   if (t0 >= t1) return;
   auto emit = [&](uint32_t p, uint32_t j, uint32_t i, float v) {
     if (plain_out) {
-      plain_out[(size_t)p * 2 * k + j] = i;
-      plain_out[(size_t)p * 2 * k + k + j] = __float_as_uint(v);
+      plain_out[(size_t)p * cw + j] = i;
+      if (w16) {
+        uint16_t* h = reinterpret_cast<uint16_t*>(plain_out + (size_t)p * cw + k);
+        h[j] = __half_as_ushort(__float2half_rn(v));
+        if ((k & 1u) && j == k - 1) h[k] = 0u;  // the chunk's padding half
+      }
+      else
+        plain_out[(size_t)p * cw + k + j] = __float_as_uint(v);
     }
   };
   for (uint32_t p = warp; p < nchunks; p += WARPS) {
@@ -1833,6 +1882,17 @@ __global__ void __launch_bounds__(THREADS) k_sgd_update(float* __restrict__ w, c
   }
   for (uint64_t i = n4 * 4 + (uint64_t)blockIdx.x * THREADS + threadIdx.x; i < n; i += stride)
     w[i] = __fsub_rn(w[i], __fmul_rn(lr, out[i]));
+}
+
+// FP16 wire (F3): pack a selection into [idx k | binary16 val k (padded)] (values already fp16-exact)
+__global__ void k_pack16(const uint32_t* __restrict__ idx, const float* __restrict__ val, uint32_t* __restrict__ out,
+                         uint64_t k) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < k) {
+    out[j] = idx[j];
+    reinterpret_cast<uint16_t*>(out + k)[j] = __half_as_ushort(__float2half_rn(val[j]));
+  }
+  if (j == 0 && (k & 1)) reinterpret_cast<uint16_t*>(out + k)[k] = 0;  // padding half
 }
 
 // Debug (TK_CHECK=1): a selection / gathered chunk must hold strictly ascending indices < n.

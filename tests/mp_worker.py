@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--rs-mode", default="ordered")
     ap.add_argument("--ag-mode", default="push")
     ap.add_argument("--select", default="mstopk")
+    ap.add_argument("--wire", default="f32")
     ap.add_argument("--sgd", type=float, default=0.0, help="also run Eq. 1's fused update with this lr")
     ap.add_argument("--zero-copy", action="store_true", help="write g into the context's input buffer")
     ap.add_argument("--out", required=True)
@@ -50,7 +51,8 @@ def main():
     log("uid ok")
     n = a.group_size
     ctx = tk.Context(a.dim, rho=a.rho, n_iters=a.n_iters, nranks=ws, rank=rank, group_size=n, seed=99, uid=uid,
-                     step4=a.step4, rs_mode=a.rs_mode, ag_mode=a.ag_mode, device=local, select=a.select)
+                     step4=a.step4, rs_mode=a.rs_mode, ag_mode=a.ag_mode, device=local, select=a.select,
+                     wire=a.wire)
     L, k = ctx.seg_len, ctx.k
     log("ctx ok", L, k)
     chunks = ws if n == 1 else ws // n
@@ -66,7 +68,7 @@ def main():
         if inbuf is not None:
             inbuf.copy_(g)
             g = inbuf
-        gat = torch.empty(chunks * 2 * k, dtype=torch.int32, device="cuda")
+        gat = torch.empty(chunks * ctx.chunk_words, dtype=torch.int32, device="cuda")
         if a.sgd:
             out = torch.empty(a.dim, dtype=torch.float32, device="cuda")
             ctx.step_sgd(g, r, wd, a.sgd, out=out, gathered=gat)
@@ -86,11 +88,12 @@ def main():
             import oracle
             grads = [gradgen.gradient(a.dim, a.dist, cfg=40, rank=p, step=step) for p in range(ws)]
             if n == 1:
-                ref = oracle.flat_step(grads, r_ref, a.rho, a.n_iters, seed=99, step=step, selector=a.select)
+                ref = oracle.flat_step(grads, r_ref, a.rho, a.n_iters, seed=99, step=step, selector=a.select,
+                                       wire=a.wire)
                 ref_gat = [ref.gathered] * ws
             else:
                 ref = oracle.hitopk_step(grads, r_ref, ws // n, n, a.rho, a.n_iters, seed=99, step=step,
-                                         selector=a.select)
+                                         selector=a.select, wire=a.wire)
                 ref_gat = [ref.column_gathered[p % n] for p in range(ws)]
             rec = {"step": step}
             rec["out_equal"] = [bool(np.array_equal(o.cpu().numpy().view(np.uint32), ref.out.view(np.uint32)))

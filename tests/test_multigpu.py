@@ -94,3 +94,10 @@ def test_exact_selector_multi_gpu(P, n, tmp_path):
 def test_fused_sgd_update_multi_gpu(P, n, step4, tmp_path):
     """Eq. 1's update fused into the decompression (flat), or after the row all-gather (dense step 4)"""
     _run(P, tmp_path, dim=8 * 131_076, rho=0.001, group_size=n, step4=step4, sgd=0.05, steps=3)
+
+
+@pytest.mark.parametrize("P,n,ag,step4", [(2, 1, "push", "dense"), (4, 1, "push", "dense"), (2, 1, "nccl", "dense"),
+                                          (4, 2, "push", "dense"), (4, 2, "push", "sparse")])
+def test_fp16_wire_multi_gpu(P, n, ag, step4, tmp_path):
+    """FP16 wire values (F3) through the fused push all-gather, NCCL and HiTopKComm"""
+    _run(P, tmp_path, dim=1_049_616, rho=0.001, group_size=n, ag_mode=ag, step4=step4, wire="f16", steps=3)

@@ -431,3 +431,44 @@ def test_sgd_update_closed_forms_and_exact_rounding():
     prod = (np.float64(lr) * g.astype(np.float64)).astype(np.float32)
     want = (w.astype(np.float64) - prod.astype(np.float64)).astype(np.float32)
     assert np.array_equal(oracle.sgd_update(w, g, float(lr)).view(np.uint32), want.view(np.uint32))
+
+
+# ---------------------------------------------------------------- FP16 wire values (F3)
+def test_fp16_wire_rounding_known_values():
+    """binary16 round-to-nearest-even of the sent value (Q31), against hand-derived bit patterns"""
+    x = np.array([1 / 3, -2.0, 65519.0, 1e5, -1e5, 2.0 ** -24 * 0.75, 1.0 + 2.0 ** -11, 1.0 + 3 * 2.0 ** -11],
+                 np.float32)
+    c = oracle.compress(x, None, len(x), 5, error_feedback=False, wire="f16")
+    h = c.sent.astype(np.float16).view(np.uint16).tolist()
+    # 1/3 -> 0x3555; -2 -> 0xC000; 65519 -> 65504 (0x7BFF, RN); +-1e5 clamp -> +-65504;
+    # 0.75 * 2^-24 -> 2^-24 (0x0001, RN); 1 + 2^-11 -> 1 (tie to even, 0x3C00); 1 + 3*2^-11 -> 1 + 2^-9 (0x3C02)
+    assert h == [0x3555, 0xC000, 0x7BFF, 0x7BFF, 0xFBFF, 0x0001, 0x3C00, 0x3C02]
+
+
+def test_fp16_wire_residual_and_layout():
+    d, k = 3001, 101
+    g = gradgen.gradient(d, "G", cfg=23)
+    r = gradgen.gradient(d, "G", cfg=24) * np.float32(0.1)
+    c = oracle.compress(g, r, k, 10, wire="f16")
+    c32 = oracle.compress(g, r, k, 10)
+    assert c.sel.idx.tolist() == c32.sel.idx.tolist()          # the selection itself is unchanged
+    ii = c.sel.idx.astype(np.int64)
+    # Sterbenz: sent is within a factor 2 of v in the normal range, so v - sent is exact and
+    # r' + sent reconstructs acc bit for bit
+    assert np.array_equal((c.residual[ii] + c.sent).view(np.uint32), c.acc[ii].view(np.uint32))
+    w = oracle.pack(c.sel.idx, c.sent, "f16")
+    assert len(w) == k + (k + 1) // 2 == oracle.chunk_words(k, "f16")
+    assert w[:k].tolist() == c.sel.idx.tolist()
+    assert w[k:].view(np.float16)[:k].astype(np.float32).tolist() == c.sent.tolist()
+    out = oracle.decompress(w, 1, k, d, "f16")
+    assert np.array_equal(out[ii], c.sent) and np.count_nonzero(out) == np.count_nonzero(c.sent)
+
+
+def test_fp16_wire_density_one_is_dense_sum_of_rounded_values():
+    d, P = 200, 3
+    gs = [gradgen.gradient(d, "G", cfg=25, rank=p) for p in range(P)]
+    res = oracle.flat_step(gs, [np.zeros(d, np.float32)] * P, 1.0, 5, wire="f16")
+    want = np.zeros(d, np.float32)
+    for p in range(P):
+        want = (want + gs[p].astype(np.float16).astype(np.float32)).astype(np.float32)
+    assert np.array_equal(res.out.view(np.uint32), want.view(np.uint32))
