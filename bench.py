@@ -57,6 +57,8 @@ def parse():
                     help="selector: MSTopK (Alg. 1) or the exact top-k of Eq. 2 (SURVEY F1)")
     ap.add_argument("--wire", default="f32", choices=["f32", "f16"],
                     help="value format on the wire: fp32 or binary16 (SURVEY F3, Fig. 7's FP16)")
+    ap.add_argument("--sgd", type=float, default=0.0,
+                    help="lr > 0: time tk_step_sgd (Eq. 1's update fused into the decompression, SURVEY F4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no soak, no e2e, no cpu baseline")
@@ -237,10 +239,10 @@ def run_reference(a, ws, rank, emit):
 def stage_bytes(name, L, d, k, P, ef, chunks):
     """Algorithmic HBM bytes of ONE launch of a stage."""
     if name == "k_compress":
-        # the design's minimum: the EF pass (read g, read r, write acc), one count pass over acc,
-        # the k (index, value) pairs and the k residual zeros; the later passes and the selection
-        # read only the compacted entries (data dependent, not counted)
-        return (12 if ef else 4) * L + 4 * L + 8 * k + (4 * k if ef else 0)
+        # the floor of any correct implementation: the EF pass (read g, read r, write acc - or read
+        # g without EF), the k (index, value) pairs and the k residual writes.  This design moves
+        # only that plus the compacted entries (~0.4 % of n, data dependent, not counted)
+        return (12 if ef else 4) * L + 8 * k + (4 * k if ef else 0)
     if name == "k_decompress":
         return 4 * d + 8 * chunks * k
     if name == "k_tile_ranges":
@@ -295,6 +297,7 @@ def main():
         r = torch.zeros(L, dtype=torch.float32, device="cuda")
         r_soak = torch.zeros(L, dtype=torch.float32, device="cuda")
         out = torch.empty(a.d, dtype=torch.float32, device="cuda")
+        w = torch.randn(a.d, generator=gen, device="cuda", dtype=torch.float32) if a.sgd else None
     stream.synchronize()
     cursor = [0]
     log("inputs generated")
@@ -302,7 +305,10 @@ def main():
     def run(steps, rr=None):
         rr = r if rr is None else rr
         for _ in range(steps):
-            ctx.step(gs[cursor[0] % nbuf], rr, out)
+            if a.sgd:  # F4: Eq. 1's update fused into the decompression (no dense aggregate written)
+                ctx.step_sgd(gs[cursor[0] % nbuf], rr, w, a.sgd)
+            else:
+                ctx.step(gs[cursor[0] % nbuf], rr, out)
             cursor[0] += 1
 
     sampler = None if a.ncu else ClockSampler(local)
@@ -378,8 +384,8 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_launch,
                 "ms_per_launch": stages[dom]["ms_per_launch"],
-                "note": "achieved = algorithmic bytes per launch (the design minimum: 16 B/elem + 12 B/pair) / "
-                        "mean CUDA-event duration of that launch inside the profiled steps"}
+                "note": "achieved = algorithmic bytes per launch (the floor: 12 B/elem (EF: read g, r; write acc) "
+                        "+ 12 B/pair) / mean CUDA-event duration of that launch inside the profiled steps"}
 
     # end-to-end through the public host-buffer API: pinned H2D of g + D2H of the gathered pairs
     e2e = None
@@ -411,7 +417,7 @@ def main():
                 "config": {"workload": workload_name(a, P), "d": a.d, "rho": a.rho, "k": k, "n_iters": a.n_iters,
                            "P": P, "group_size": n, "step4": a.step4 if n > 1 else None, "dist": a.dist,
                            "allgather": (a.ag_mode if n == 1 and P > 1 else None), "selector": a.select,
-                           "wire": a.wire,
+                           "wire": a.wire, "fused_sgd_lr": a.sgd or None,
                            "levels_per_pass": a.levels or 10, "input_buffers": nbuf,
                            "inputs": "fresh seeded N(0,1) gradient per step (torch CUDA generator, pre-generated in "
                                      "HBM); residual carried from r=0 at step 0; timed steps W..W+K-1",
