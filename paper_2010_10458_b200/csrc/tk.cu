@@ -42,7 +42,8 @@ struct tk_ctx {
   uint32_t ef_compact = 1;            // compaction in the ef phase (TK_EF_COMPACT=0 disables; bits unchanged)
   int lev_sched[NMAX];
   uint32_t units_per_warp = 1;        // ef phase: aligned power-of-two run of 512-element units per warp
-  uint32_t* cta_cls = nullptr;        // [2][grid] per-CTA class counts
+  uint32_t* cta_cls = nullptr;        // [4][grid] per-CTA class counts, entries
+  uint32_t* cta_suffix = nullptr;     // [grid][HIST_BINS] per-CTA histogram suffix sums
   uint32_t* totals = nullptr;         // [npass][HREP][256] pass totals / histograms
   uint32_t* bar = nullptr;            // grid barrier words [2] + flags [2]
   uint32_t* flags = nullptr;
@@ -177,6 +178,7 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.wcnt = c->wcnt;
   f.totals = c->totals;
   f.cta_cls = c->cta_cls;
+  f.cta_suffix = c->cta_suffix;
   f.bar = c->bar;
   f.flags = c->flags;
   f.cp = c->cp;
@@ -281,6 +283,7 @@ tk_status plan_launches(tk_ctx* c) {
   TK_TRY(dev_alloc(c, &c->cta_sum, c->grid));
   TK_TRY(dev_alloc(c, &c->cta_max, c->grid));
   TK_TRY(dev_alloc(c, &c->cta_cls, 4 * (size_t)c->grid));
+  TK_TRY(dev_alloc(c, &c->cta_suffix, (size_t)c->grid * HIST_BINS));
   TK_TRY(dev_alloc(c, &c->totals, (size_t)HIST_BINS * HREP * c->npass));
   TK_TRY(dev_alloc(c, &c->bar, 8));
   TK_CUDA(c, cudaMemset(c->bar, 0, 8 * sizeof(uint32_t)));
@@ -347,7 +350,8 @@ tk_status open_push_peers(tk_ctx* c) {
 }
 
 void free_all(tk_ctx* c) {
-  void* ptrs[] = {c->cp.idx, c->cp.bits, c->cp.cnt, c->cta_sum, c->cta_max, c->cta_cls, c->totals, c->bar, c->wcnt,
+  void* ptrs[] = {c->cp.idx, c->cp.bits, c->cp.cnt, c->cta_sum, c->cta_max, c->cta_cls, c->cta_suffix, c->totals,
+                  c->bar, c->wcnt,
                   c->ctrl, c->send, c->recv,
                   c->recv_row, c->seg, c->h_g, c->h_r, c->h_out};
   for (void* p : ptrs)

@@ -926,8 +926,12 @@ struct HistSmem {
   uint32_t h[HIST_BINS];  // the CTA's histogram (shared-memory atomics; entries spread over the bins)
 };
 
+// suf (optional): this CTA's suffix sums S[b] = sum_{b' >= b} h[b'] of its own histogram, so that
+// after the replay each CTA can read the class counts of the CTAs before it without another
+// grid barrier (#entries of CTA c at or above candidate s = S_c[s + 1]).
 template <int LEV>
-__device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uint32_t* ghist, HistSmem& hs) {
+__device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uint32_t* ghist, HistSmem& hs,
+                                           uint32_t* suf = nullptr) {
   constexpr int NB = 1 << LEV;
   const int32_t* s_key = reinterpret_cast<const int32_t*>(sc->cand_key);  // sorted, in shared memory
   uint32_t* s_h = hs.h;
@@ -966,6 +970,24 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
   for (int b = threadIdx.x; b < NB; b += THREADS) {
     const uint32_t t = s_h[b];
     if (b > 0 && t) atomicAdd(ghist + (blockIdx.x & (HREP - 1)) * TOT_STRIDE + b, t);  // bucket 0 is never needed
+  }
+  if (suf) {
+    __shared__ uint32_t s_sw[WARPS];
+    uint32_t v[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int b = NB - 1 - (4 * (int)threadIdx.x + q);
+      v[q] = b >= 0 ? s_h[b] : 0u;
+      sum += v[q];
+    }
+    uint32_t total;
+    uint32_t acc = block_excl_scan(sum, s_sw, total);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int b = NB - 1 - (4 * (int)threadIdx.x + q);
+      acc += v[q];
+      if (b >= 0) suf[b] = acc;
+    }
   }
   __syncthreads();
 }
@@ -1239,6 +1261,7 @@ struct Fused {
   int max_pass;              // passes for which totals / wcnt are allocated
   uint32_t ef_compact;       // 1: compact in the ef phase at the key the previous call predicted
   uint16_t* val16_out;       // FP16 wire: binary16 values of the selection (nullptr: none)
+  uint32_t* cta_suffix;      // [grid][HIST_BINS] per-CTA histogram suffix sums (barrier-free prefix)
   uint32_t wire16;           // FP16 wire values (F3): round the values sent, keep the error in r
 };
 
@@ -1333,6 +1356,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   stats_root(f.cta_sum, f.cta_max, f.sp, &sc, f.step, f.lev0);
   stamp();
   const bool ef_ok = efk > 0u && __ldcg(f.flags + 2) == 0u;  // entries = {a >= efk}, none dropped
+  bool nobar = false;  // the cross-CTA prefix comes from the published histogram suffixes (no barrier)
   if (tid == 0) { sc.cmp_bottom = 0u; sc.cap_ok = 0u; sc.ef_used = 0u; sc.nnz_lb = 0ull; }
   __syncthreads();
   if constexpr (SEL == SEL_EXACT) {
@@ -1505,6 +1529,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   // the rest, each further pass is a histogram pass on them, else it resolves up to 2 levels on
   // the whole vector.  The bits do not depend on this schedule. ----
   const int N = (int)f.n_iters;
+  const bool single = N <= min(HIST_LEV, f.cap_levels);  // the fast search resolves all N levels in one pass
   __shared__ int s_got;
   auto search = [&](int p0, bool fast) -> int {
     int done = 0;
@@ -1518,6 +1543,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       bool hist = false;
       uint32_t* tot_p = f.totals + HIST_BINS * HREP * p;
       const bool first = (p == p0) && !fast;
+      // the fast search's single pass also publishes this CTA's histogram suffix sums
+      uint32_t* suf = (fast && single) ? f.cta_suffix + (size_t)blockIdx.x * HIST_BINS : nullptr;
       if (first) {
         lev = f.lev0;  // keys along the predicted path
         if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, p);
@@ -1527,16 +1554,16 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         hist = true;
         lev = min(min(HIST_LEV, f.cap_levels), N - done);
         switch (lev) {
-          case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist); break;
-          case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist); break;
-          case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist); break;
-          case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist); break;
-          case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist); break;
-          case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist); break;
-          case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist); break;
-          case 8: hist_phase<8>(&sc, f.cp, tot_p, s_hist); break;
-          case 9: hist_phase<9>(&sc, f.cp, tot_p, s_hist); break;
-          default: hist_phase<10>(&sc, f.cp, tot_p, s_hist); break;
+          case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 8: hist_phase<8>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 9: hist_phase<9>(&sc, f.cp, tot_p, s_hist, suf); break;
+          default: hist_phase<10>(&sc, f.cp, tot_p, s_hist, suf); break;
         }
       } else {
         lev = min(min(2, f.cap_levels), N - done);
@@ -1584,6 +1611,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     __syncthreads();
     ok = s_got != 0;
   }
+  nobar = ok && single;
   if (!ok) {
     if (tid == 0) {
       search_reset(&sc, f.sp.n);
@@ -1649,20 +1677,35 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     s_w[1][warp] = c2;
   }
   __syncthreads();
-  if (tid == 0) {
-    uint32_t t1 = 0, t2 = 0, tn = 0;
-    for (int w = 0; w < WARPS; ++w) { t1 += s_w[0][w]; t2 += s_w[1][w]; tn += s_ne[w]; }
-    f.cta_cls[blockIdx.x] = t1;
-    f.cta_cls[gridDim.x + blockIdx.x] = t2;
-    f.cta_cls[2 * gridDim.x + blockIdx.x] = tn;  // compacted entries (statistics)
+  if (!nobar) {
+    if (tid == 0) {
+      uint32_t t1 = 0, t2 = 0, tn = 0;
+      for (int w = 0; w < WARPS; ++w) { t1 += s_w[0][w]; t2 += s_w[1][w]; tn += s_ne[w]; }
+      f.cta_cls[blockIdx.x] = t1;
+      f.cta_cls[gridDim.x + blockIdx.x] = t2;
+      f.cta_cls[2 * gridDim.x + blockIdx.x] = tn;  // compacted entries (statistics)
+    }
+    grid_sync(f.bar);
   }
-  grid_sync(f.bar);
   stamp();
   {
     uint32_t a1 = 0, a2 = 0;
-    for (uint32_t b = tid; b < blockIdx.x; b += THREADS) {
-      a1 += __ldcg(f.cta_cls + b);
-      a2 += __ldcg(f.cta_cls + gridDim.x + b);
+    if (nobar) {
+      // class counts of the CTAs before this one, from their published histogram suffixes: key1 /
+      // key2 are candidates s1 / s2 of the single pass (prov = pass 0 * TMAX + s)
+      const int s1 = sc.prov1, s2 = sc.prov2;
+      for (uint32_t b = tid; b < blockIdx.x; b += THREADS) {
+        const uint32_t* S = f.cta_suffix + (size_t)b * HIST_BINS;
+        const uint32_t x1 = s1 >= 0 ? __ldcg(S + s1 + 1) : 0u;
+        const uint32_t xa = __ldcg(S + s2 + 1);
+        a1 += x1;
+        a2 += xa - x1;
+      }
+    } else {
+      for (uint32_t b = tid; b < blockIdx.x; b += THREADS) {
+        a1 += __ldcg(f.cta_cls + b);
+        a2 += __ldcg(f.cta_cls + gridDim.x + b);
+      }
     }
     a1 = __reduce_add_sync(0xffffffffu, a1);
     a2 = __reduce_add_sync(0xffffffffu, a2);
@@ -1711,7 +1754,10 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   }
   if (blockIdx.x == 0) {
     uint32_t tn = 0;
-    for (uint32_t b = tid; b < gridDim.x; b += THREADS) tn += __ldcg(f.cta_cls + 2 * gridDim.x + b);
+    // entries per CTA: from the ef phase (written before the first barrier) when the prefix ran
+    // without a barrier, else from the prefix phase
+    const uint32_t* ent = nobar ? cta_ent : f.cta_cls + 2 * gridDim.x;
+    for (uint32_t b = tid; b < gridDim.x; b += THREADS) tn += __ldcg(ent + b);
     tn = __reduce_add_sync(0xffffffffu, tn);
     if (lane == 0) s_w[0][warp] = tn;
     __syncthreads();
