@@ -83,6 +83,7 @@ struct Ctrl {
   uint32_t xlo, xhi, xcnt_lo, xcnt_hi;
   uint32_t prev_T, prev_dT;  // the previous call's T and how far T moved in that call
   uint32_t xretry;       // a whole-vector compaction retry was spent
+  uint32_t xguess;       // exact: upper end of the first histogram pass's keys (0: xhi)
   uint32_t cmp_bottom;   // the entries sit at the bottom of the warp regions (ef-phase compaction)
   uint32_t ef_key;       // compaction key of the NEXT call's ef phase (0: none), set at the end of a call
   uint32_t ef_used;      // this call's selection ran on the ef-phase entries
@@ -1319,7 +1320,10 @@ __device__ __forceinline__ void exact_update(Ctrl* c, const uint32_t* keys, cons
 // nk keys splitting (xlo, xhi] evenly: xlo + ceil(j * w / (nk + 1)), j = 1..nk (ascending; with
 // w <= nk + 1 they cover every key of the bracket, so a pass always narrows it)
 __device__ __forceinline__ uint32_t exact_split(const Ctrl* c, uint32_t j, uint32_t parts) {
-  const uint64_t w = (uint64_t)c->xhi - c->xlo;
+  // the first histogram pass after the EF-pass compaction spans only the predicted neighbourhood
+  // [xlo, xguess] of T (keys above it count < k or not, either way the bracket narrows)
+  const uint32_t hi = (c->xguess > c->xlo && c->xguess < c->xhi) ? c->xguess : c->xhi;
+  const uint64_t w = (uint64_t)hi - c->xlo;
   return c->xlo + (uint32_t)((j * w + parts - 1) / parts);
 }
 
@@ -1380,10 +1384,16 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       sc.xlo = 0u; sc.xcnt_lo = (uint32_t)f.sp.n;
       sc.xhi = min(sc.umax_bits, 0x7FFFFFFFu) + 1u; sc.xcnt_hi = 0u;
       sc.xretry = 0u;
+      sc.xguess = 0u;
       sc.it = 0u;
       if (ef_ok && (uint64_t)s_e >= k && efk < sc.xhi) {
         // T >= efk: the ef-phase entries hold every element the narrowing and the selection need
         sc.xlo = efk; sc.xcnt_lo = s_e;
+        // T is expected near the previous T moved once more by its last move (error feedback
+        // keeps it rising): the first histogram pass spans [efk, P + 2 * move + margin]
+        const uint32_t P = sc.prev_T;
+        const uint32_t mv = min(sc.prev_dT, 1u << 22);
+        sc.xguess = (P > efk) ? P + 2u * mv + (1u << 12) : 0u;
         sc.cap_ok = 1u; sc.cmp_bottom = 1u; sc.ef_used = 1u;
       }
     }
@@ -1472,6 +1482,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
           }
           if (lo >= 0) { sc.xlo = sc.cand_key[lo]; sc.xcnt_lo = s_tot[lo]; }
           if (hi < HIST_BINS - 1) { sc.xhi = sc.cand_key[hi]; sc.xcnt_hi = s_tot[hi]; }
+          sc.xguess = 0u;
         } else {
           exact_update(&sc, sc.cand_key, s_tot, 3, k);
           if (mode == 1) sc.cap_ok = (__ldcg(f.flags + 1) == 0u) ? 1u : 0u;
