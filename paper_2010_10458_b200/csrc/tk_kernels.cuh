@@ -613,27 +613,26 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
         // the unit's hits go to the warp's shared-memory staging buffer (or, if more than it
         // holds, straight to the entries)
         const bool direct = tu > SCAP;
-        uint32_t cb = direct ? flushed : staged;
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t pos = cb + ((excl >> (8 * ch)) & 0xFFu);
-          const uint32_t w4[4] = {__float_as_uint(acc[ch].x), __float_as_uint(acc[ch].y), __float_as_uint(acc[ch].z),
-                                  __float_as_uint(acc[ch].w)};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (m & (1u << (4 * ch + e))) {
-              const uint32_t i = (uint32_t)(u * ROUND + ch * 128 + 4 * lane + e);
-              if (direct) {
-                if (pos < cp.C) { oi[pos] = i; ob[pos] = w4[e]; }
-              } else {
-                TK_DCHECK(pos < SCAP, "ef-stage", pos, staged);
-                s_si[warp][pos] = i;
-                s_sb[warp][pos] = w4[e];
-              }
-              ++pos;
-            }
+        const uint32_t b0 = direct ? flushed : staged;
+        const uint32_t t0 = tot & 0xFFu, t1 = (tot >> 8) & 0xFFu, t2 = (tot >> 16) & 0xFFu;
+        // only this lane's hits are visited (usually none or one): chunk ch's run starts at
+        // b0 + hits of the earlier chunks, then the earlier lanes' hits of chunk ch, then this
+        // lane's earlier hits in the chunk
+        for (uint32_t mm = m; mm; mm &= mm - 1u) {
+          const int j = __ffs(mm) - 1;
+          const int ch = j >> 2, e = j & 3;
+          const uint32_t cbase = b0 + (ch > 0 ? t0 : 0u) + (ch > 1 ? t1 : 0u) + (ch > 2 ? t2 : 0u);
+          const uint32_t pos = cbase + ((excl >> (8 * ch)) & 0xFFu) + __popc(m & ((1u << j) - 1u) & (0xFu << (4 * ch)));
+          const float4 a4 = ch == 0 ? acc[0] : (ch == 1 ? acc[1] : (ch == 2 ? acc[2] : acc[3]));
+          const float av = e == 0 ? a4.x : (e == 1 ? a4.y : (e == 2 ? a4.z : a4.w));
+          const uint32_t i = (uint32_t)(u * ROUND + ch * 128 + 4 * lane + e);
+          if (direct) {
+            if (pos < cp.C) { oi[pos] = i; ob[pos] = __float_as_uint(av); }
+          } else {
+            TK_DCHECK(pos < SCAP, "ef-stage", pos, staged);
+            s_si[warp][pos] = i;
+            s_sb[warp][pos] = __float_as_uint(av);
           }
-          cb += (tot >> (8 * ch)) & 0xFFu;
         }
         if (direct) flushed += tu; else staged += tu;
         __syncwarp();
