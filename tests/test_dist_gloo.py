@@ -70,27 +70,31 @@ def test_unique_id_broadcast():
 D, RHO, N, STEPS = 20_008, 0.01, 10, 3
 
 
-def _flat(rank, ws):
+def _flat(selector, wire, rank, ws):
     r = np.zeros(D, np.float32)
     outs = []
+    k = oracle.k_from_density(D, RHO)
     for step in range(STEPS):
         g = gradgen.gradient(D, "G", cfg=50, rank=rank, step=step)
-        c = oracle.compress(g, r, oracle.k_from_density(D, RHO), N, seed=3, step=step, rank=rank)
-        chunk = torch.from_numpy(oracle.pack(c.sel.idx, c.sel.val).view(np.int32))
+        c = oracle.compress(g, r, k, N, seed=3, step=step, rank=rank, selector=selector, wire=wire)
+        chunk = torch.from_numpy(oracle.pack(c.sel.idx, c.sent, wire).view(np.int32))
         gathered = [torch.empty_like(chunk) for _ in range(ws)]
         dist.all_gather(gathered, chunk)
         g_all = torch.cat(gathered).numpy().view(np.uint32)
-        outs.append(oracle.decompress(g_all, ws, oracle.k_from_density(D, RHO), D).view(np.uint32).tobytes())
+        outs.append(oracle.decompress(g_all, ws, k, D, wire).view(np.uint32).tobytes())
         r = c.residual
     return outs
 
 
-def test_flat_decomposition_matches_simulation():
-    out = _spawn(_flat)
+@pytest.mark.parametrize("selector,wire", [("mstopk", "f32"), ("exact", "f32"), ("mstopk", "f16")])
+def test_flat_decomposition_matches_simulation(selector, wire):
+    """the per-rank compress / packed all-gather / rank-ordered decompress decomposition (also with the
+    exact selector, F1, and FP16 wire values, F3) reproduces the single-process simulation"""
+    out = _spawn(functools.partial(_flat, selector, wire))
     r = [np.zeros(D, np.float32) for _ in range(2)]
     for step in range(STEPS):
         gs = [gradgen.gradient(D, "G", cfg=50, rank=p, step=step) for p in range(2)]
-        ref = oracle.flat_step(gs, r, RHO, N, seed=3, step=step)
+        ref = oracle.flat_step(gs, r, RHO, N, seed=3, step=step, selector=selector, wire=wire)
         for rank in range(2):
             assert out[rank][step] == ref.out.view(np.uint32).tobytes()
         r = [c.residual for c in ref.per_rank]
