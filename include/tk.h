@@ -10,6 +10,11 @@
  *   rank-ordered index accumulation (decompress)     — Alg. 2 l.15-20
  *   residual write-back of the unsent mass           — BASELINE.json north_star
  *   HiTopKComm (m x n virtual nodes), Algorithm 2    — P:203-248
+ * and the adjacent rows of SURVEY.md §8(f):
+ *   exact top-k selector (TK_SELECT_EXACT)           — Eq. 2, P:131-139 (F1)
+ *   fused all-gather pushed over NVLink (TK_AG_PUSH) — P:197 (F2)
+ *   FP16 values on the wire (TK_WIRE_F16)            — Fig. 7 ran FP16, P:337 (F3)
+ *   SGD update fused into decompression (tk_step_sgd)— Eq. 1, P:65-67 (F4)
  * "Q<n>" refers to the numbered readings of silent/ambiguous passages in DESIGN.md.
  *
  * Conventions (all entry points):
@@ -104,7 +109,7 @@ typedef struct tk_config {
 typedef struct tk_stats {
   double mean;             /* a-bar, canonical fp64 pairwise mean of |acc| (Alg. 1 l.2, Q3)    */
   uint32_t max_bits;       /* bits of u = max |acc| (Alg. 1 l.3)                               */
-  uint32_t n_trials;       /* = N                                                              */
+  uint32_t n_trials;       /* = N (MSTopK); the narrowing passes (exact selector, no trial log) */
   double ratio[52];        /* per trial: ratio (Alg. 1 l.8)                                    */
   double thres[52];        /*            thres (l.9, fp64, Q4)                                 */
   uint32_t key[52];        /*            bits of the smallest fp32 >= thres                    */
