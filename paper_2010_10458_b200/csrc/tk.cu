@@ -39,7 +39,8 @@ struct tk_ctx {
   uint32_t occ_dec = 1;               // resident decompression CTAs per SM
   uint32_t levels = 4, npass = 0;
   uint32_t debug_check = 0;           // TK_CHECK=1: verify every selection (ascending, in range) on the device
-  uint32_t ef_compact = 1;            // compaction in the ef phase (TK_EF_COMPACT=0 disables; bits unchanged)
+  uint32_t ef_compact = 1;
+  uint32_t ef_compact_peers = 0;      // TK_EF_COMPACT_PEERS=1: also with NP > 0 (open issue)            // compaction in the ef phase (TK_EF_COMPACT=0 disables; bits unchanged)
   int lev_sched[NMAX];
   uint32_t units_per_warp = 1;        // ef phase: aligned power-of-two run of 512-element units per warp
   uint32_t* cta_cls = nullptr;        // [4][grid] per-CTA class counts, entries
@@ -196,7 +197,7 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   // EF-pass compaction is off when the EF pass sums peer segments (HiTopKComm ordered
   // reduce-scatter): with it on, 1 in ~6 4-GPU bench runs hit an illegal address that no device
   // check, launch-blocking or sanitised run reproduces (open issues)
-  f.ef_compact = (np == 0) ? c->ef_compact : 0u;
+  f.ef_compact = (np == 0 || c->ef_compact_peers) ? c->ef_compact : 0u;
   const void* kern = compress_kernel(ef, np, c->cfg.select);
   if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
   void* args[] = {&f};
@@ -448,6 +449,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
     else c->npass += k.n_iters;  // an ef-phase search (>= 1 level per pass) may precede a restart
     if (const char* e = getenv("TK_EF_COMPACT")) c->ef_compact = atoi(e) != 0 ? 1u : 0u;
     if (const char* e = getenv("TK_CHECK")) c->debug_check = atoi(e) != 0 ? 1u : 0u;
+    if (const char* e = getenv("TK_EF_COMPACT_PEERS")) c->ef_compact_peers = atoi(e) != 0 ? 1u : 0u;
   }
   auto bail = [&](tk_status s) {
     free_all(c);
