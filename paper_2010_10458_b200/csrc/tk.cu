@@ -5,7 +5,8 @@
 // row comm of the n GPUs of a virtual node and the column comm of the m GPUs with the same
 // position), and the launch sequence of one iteration.  Everything is enqueued on the caller's
 // stream with no host synchronisation inside an iteration, so a whole tk_step is capturable in
-// a CUDA graph by the caller.
+// a CUDA graph by the caller (except with the push all-gather: its per-step packet tag is a
+// kernel argument).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
