@@ -17,7 +17,7 @@ from dataclasses import dataclass
 
 import torch  # loads the venv's libnccl.so.2 first; libtk links the same soname
 
-__all__ = ["Context", "TkError", "k_from_density", "unique_id", "broadcast_unique_id", "lib_path", "STATUS"]
+__all__ = ["Context", "Bucket", "bucket_layout", "TkError", "k_from_density", "unique_id", "broadcast_unique_id", "lib_path", "STATUS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libtk.so")
@@ -346,3 +346,72 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------------------------------
+# Bucketed multi-tensor step (SURVEY F4, second half): the "tensor fusion" the paper names as
+# the way gradient communication overlaps backpropagation (P:114, §2.2), reading Q32 of DESIGN.md: a bucket is the concatenation of its layers' gradients in list order, and
+# one tk_step runs on it — one MSTopK selection over the fused d = sum d_l with k = rho * d
+# (P:197), one sparse all-gather, one decompression.  The layers are zero-copy views of the
+# bucket's flat buffers, so fusion costs no copy pass; this module only computes offsets.
+
+def bucket_layout(shapes) -> list:
+    """[(offset, numel, shape)] of each layer in the fused flat buffer: contiguous, in list
+    order, no padding (padding would add zeros to the mean of Alg. 1 l.2)."""
+    out, off = [], 0
+    for s in shapes:
+        shape = (int(s),) if isinstance(s, int) else tuple(int(x) for x in s)
+        if any(x < 0 for x in shape):
+            raise ValueError(f"negative dimension in layer shape {shape}")
+        n = 1
+        for x in shape:
+            n *= x
+        out.append((off, n, shape))
+        off += n
+    if off == 0:
+        raise ValueError("a bucket needs at least one element")
+    if off >= 1 << 32:
+        raise ValueError("a bucket holds < 2^32 elements (u32 indices on the wire, Q15)")
+    return out
+
+
+class Bucket:
+    """Many layers, one tk_step.  ``grads[i]`` / ``outputs[i]`` are views (layer shapes) of the
+    flat gradient / aggregate buffers; write the layer gradients into ``grads`` (or let autograd
+    accumulate into them), then ``step()`` or ``step_sgd(params_flat, lr)``.  Context keyword
+    arguments (nranks, rank, uid, select, wire, group_size, ...) pass through to ``Context``."""
+
+    def __init__(self, shapes, rho: float = 0.001, n_iters: int = 10, **ctx_kwargs):
+        self.layout = bucket_layout(shapes)
+        self.d = sum(n for _, n, _ in self.layout)
+        self.ctx = Context(self.d, rho=rho, n_iters=n_iters, **ctx_kwargs)
+        dev = self.ctx.device
+        # HiTopKComm ordered mode: the gradient lives in libtk's peer-visible buffer (no copy-in)
+        flat = self.ctx.input_buffer()
+        self.flat_grad = torch.zeros(self.d, dtype=torch.float32, device=dev) if flat is None else flat
+        self.flat_grad.zero_()
+        self.residual = torch.zeros(self.d, dtype=torch.float32, device=dev)
+        self.flat_out = torch.empty(self.d, dtype=torch.float32, device=dev)
+        self.grads = self.views(self.flat_grad)
+        self.outputs = self.views(self.flat_out)
+
+    def views(self, flat):
+        """Layer-shaped views of a flat buffer of the bucket's size (e.g. the parameters)."""
+        if flat.numel() != self.d:
+            raise ValueError(f"flat buffer has {flat.numel()} elements, the bucket {self.d}")
+        return [flat[o:o + n].view(s) for o, n, s in self.layout]
+
+    def step(self):
+        """One iteration over the whole bucket; returns the layer-shaped aggregates."""
+        self.ctx.step(self.flat_grad, self.residual, out=self.flat_out)
+        return self.outputs
+
+    def step_sgd(self, params_flat, lr: float, keep_out: bool = False):
+        """One iteration plus Eq. 1's update of the bucket's flat parameter buffer, fused into
+        the decompression (tk_step_sgd)."""
+        self.ctx.step_sgd(self.flat_grad, self.residual, params_flat, lr,
+                          out=self.flat_out if keep_out else None)
+        return params_flat
+
+    def close(self):
+        self.ctx.close()
