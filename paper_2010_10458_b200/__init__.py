@@ -401,9 +401,9 @@ class Bucket:
             raise ValueError(f"flat buffer has {flat.numel()} elements, the bucket {self.d}")
         return [flat[o:o + n].view(s) for o, n, s in self.layout]
 
-    def step(self):
+    def step(self, gathered=None):
         """One iteration over the whole bucket; returns the layer-shaped aggregates."""
-        self.ctx.step(self.flat_grad, self.residual, out=self.flat_out)
+        self.ctx.step(self.flat_grad, self.residual, out=self.flat_out, gathered=gathered)
         return self.outputs
 
     def step_sgd(self, params_flat, lr: float, keep_out: bool = False):

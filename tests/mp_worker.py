@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--wire", default="f32")
     ap.add_argument("--sgd", type=float, default=0.0, help="also run Eq. 1's fused update with this lr")
     ap.add_argument("--zero-copy", action="store_true", help="write g into the context's input buffer")
+    ap.add_argument("--bucket", action="store_true", help="drive the step through tk.Bucket (3 layer views)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
 
@@ -50,13 +51,19 @@ def main():
     uid = tk.broadcast_unique_id()
     log("uid ok")
     n = a.group_size
-    ctx = tk.Context(a.dim, rho=a.rho, n_iters=a.n_iters, nranks=ws, rank=rank, group_size=n, seed=99, uid=uid,
-                     step4=a.step4, rs_mode=a.rs_mode, ag_mode=a.ag_mode, device=local, select=a.select,
-                     wire=a.wire)
+    kw = dict(n_iters=a.n_iters, nranks=ws, rank=rank, group_size=n, seed=99, uid=uid, step4=a.step4,
+              rs_mode=a.rs_mode, ag_mode=a.ag_mode, device=local, select=a.select, wire=a.wire)
+    bucket = None
+    if a.bucket:  # the same flat gradient, seen as three layers of one bucket (reading Q32)
+        q = a.dim // 3
+        bucket = tk.Bucket([(q,), (1,), (a.dim - q - 1,)], rho=a.rho, **kw)
+        ctx = bucket.ctx
+    else:
+        ctx = tk.Context(a.dim, rho=a.rho, **kw)
     L, k = ctx.seg_len, ctx.k
     log("ctx ok", L, k)
     chunks = ws if n == 1 else ws // n
-    r = torch.zeros(L, dtype=torch.float32, device="cuda")
+    r = torch.zeros(L, dtype=torch.float32, device="cuda") if bucket is None else bucket.residual
     results = []
     ok = True
     r_ref = [np.zeros(L, np.float32) for _ in range(ws)]
@@ -69,7 +76,12 @@ def main():
             inbuf.copy_(g)
             g = inbuf
         gat = torch.empty(chunks * ctx.chunk_words, dtype=torch.int32, device="cuda")
-        if a.sgd:
+        if bucket is not None:
+            for (o, cnt, _), view in zip(bucket.layout, bucket.grads):
+                view.copy_(g[o:o + cnt])
+            bucket.step(gathered=gat)
+            out = bucket.flat_out
+        elif a.sgd:
             out = torch.empty(a.dim, dtype=torch.float32, device="cuda")
             ctx.step_sgd(g, r, wd, a.sgd, out=out, gathered=gat)
         else:

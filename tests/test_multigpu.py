@@ -101,3 +101,10 @@ def test_fused_sgd_update_multi_gpu(P, n, step4, tmp_path):
 def test_fp16_wire_multi_gpu(P, n, ag, step4, tmp_path):
     """FP16 wire values (F3) through the fused push all-gather, NCCL and HiTopKComm"""
     _run(P, tmp_path, dim=1_049_616, rho=0.001, group_size=n, ag_mode=ag, step4=step4, wire="f16", steps=3)
+
+
+@pytest.mark.parametrize("P,n", [(2, 1), (4, 1), (2, 2), (4, 2)])
+def test_bucketed_step_multi_gpu(P, n, tmp_path):
+    """the bucketed multi-tensor step (reading Q32): three layer views of one bucket,
+    flat or HiTopKComm (whose bucket gradient is libtk's peer-visible input buffer)"""
+    _run(P, tmp_path, dim=8 * 131_076 if n > 1 else 1_000_003, rho=0.001, group_size=n, bucket=True, steps=3)
