@@ -390,7 +390,9 @@ class Bucket:
         flat = self.ctx.input_buffer()
         self.flat_grad = torch.zeros(self.d, dtype=torch.float32, device=dev) if flat is None else flat
         self.flat_grad.zero_()
-        self.residual = torch.zeros(self.d, dtype=torch.float32, device=dev)
+        # EF residual of this rank's part of the selection: the whole bucket (flat) or the
+        # rank's segment of length d / n (HiTopKComm, Eq. 4-5)
+        self.residual = torch.zeros(self.ctx.seg_len, dtype=torch.float32, device=dev)
         self.flat_out = torch.empty(self.d, dtype=torch.float32, device=dev)
         self.grads = self.views(self.flat_grad)
         self.outputs = self.views(self.flat_out)
