@@ -7,13 +7,14 @@ written from PAPER.md and the readings listed in DESIGN.md.  Importable only fro
 ``--impl reference``).  Shares no code with ``paper_2010_10458_b200``.
 """
 from .mstopk import (RAND_FIRST, RAND_SEEDED, CompressResult, ExactResult, MSTopKResult, ceil_f32_bits,
-                     compress, exact_select, exact_topk, k_from_density, magnitudes, mstopk, pairwise_sum_f64)
+                     compress, exact_select, exact_topk, k_from_density, magnitudes, mstopk, mstopk_prose,
+                     pairwise_sum_f64)
 from .aggregate import (FlatResult, HiTopKResult, allgather, chunk_words, decompress, flat_step, hitopk_step,
                         pack, reduce_scatter_ordered, sgd_update)
 from .rng import splitmix64, window_hash
 
 __all__ = [
     "RAND_FIRST", "RAND_SEEDED", "CompressResult", "ExactResult", "MSTopKResult", "exact_select", "ceil_f32_bits", "compress", "exact_topk",
-    "k_from_density", "magnitudes", "mstopk", "pairwise_sum_f64", "FlatResult", "HiTopKResult", "allgather",
+    "k_from_density", "magnitudes", "mstopk", "mstopk_prose", "pairwise_sum_f64", "FlatResult", "HiTopKResult", "allgather",
     "decompress", "flat_step", "hitopk_step", "pack", "reduce_scatter_ordered", "sgd_update", "chunk_words", "splitmix64", "window_hash",
 ]

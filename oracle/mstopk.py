@@ -224,6 +224,8 @@ def compress(g: np.ndarray, r: np.ndarray | None, k: int, n_iters: int, *, seed:
         sel = exact_select(acc, k)
     elif selector == "mstopk":
         sel = mstopk(acc, k, n_iters, seed=seed, step=step, rank=rank, rand_mode=rand_mode)
+    elif selector == "prose":
+        sel = mstopk_prose(acc, k, n_iters, seed=seed, step=step, rank=rank, rand_mode=rand_mode)
     else:
         raise ValueError(f"unknown selector {selector!r}")
     if wire == "f32":
@@ -241,3 +243,75 @@ def compress(g: np.ndarray, r: np.ndarray | None, k: int, n_iters: int, *, seed:
         # Q14: the sent entries keep what was not sent: +0 (fp32 wire), fl32(v - sent) (FP16 wire)
         res[ii] = np.float32(0.0) if wire == "f32" else (sel.val - sent).astype(np.float32)
     return CompressResult(sel=sel, acc=acc, residual=res, sent=sent)
+
+
+def mstopk_prose(x: np.ndarray, k: int, n_iters: int, *, seed: int = 0, step: int = 0, rank: int = 0,
+                 rand_mode: int = RAND_SEEDED) -> MSTopKResult:
+    """MSTopK with the threshold search the PROSE describes (SURVEY F3 `TK_SEARCH_PROSE`),
+    reading Q33 of DESIGN.md, step by step in the prose's order:
+
+    - "We first use the average value (a-bar) ... as the threshold (thres1)": trial 1 is t = a-bar.
+    - "If the dimension of kappa is smaller (or larger) than k, then we half (or double) thres1 as
+      thres2 ... we repeat the above search": while no trial has yet landed on each side of the
+      k-th magnitude, the next trial is t/2 when nnz(a >= t) < k, 2t when nnz > k (exact in fp64).
+      nnz == k counts as the "not larger" side, as in Alg. 1 l.11.
+    - "then we can further narrow down the thresholds with the same pattern of search": once
+      bracketed, the next trial is the fp64 midpoint of the two bracketing thresholds.
+    - "We set a fixed number of searches (say N), and finally we select k elements using the
+      chosen two thresholds": after N trials (k1, thres1) / (k2, thres2) are updated exactly as
+      Alg. 1 l.11-20 does, and the selection is Alg. 1 l.25-29 unchanged (Q8-Q12).
+    """
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    d = x.shape[0]
+    if d < 1:
+        raise ValueError("d must be >= 1")
+    if not (1 <= k <= d):
+        raise ValueError("k must lie in [1, d]")
+    if not (1 <= n_iters <= 52):
+        raise ValueError("N must lie in [1, 52] (Q5)")
+    a = magnitudes(x)
+    if not np.all(np.isfinite(a)):
+        raise ValueError("non-finite input (Q24)")
+    a64 = a.astype(np.float64)
+    abar = pairwise_sum_f64(a) / float(d)
+    u = float(a.max())
+    k1, k2 = 0, d
+    thres1, thres2 = 0.0, 0.0
+    set1, set2 = False, False
+    t_hi = None   # smallest trial threshold seen with nnz <= k
+    t_lo = None   # largest trial threshold seen with nnz > k
+    t = abar
+    trials = []
+    for _ in range(n_iters):
+        nnz = int(np.count_nonzero(a64 >= t))
+        trials.append((float("nan"), t, ceil_f32_bits(t), nnz))
+        if nnz <= k:
+            t_hi = t if t_hi is None else min(t_hi, t)
+            if nnz > k1:
+                k1, thres1, set1 = nnz, t, True
+        else:
+            t_lo = t if t_lo is None else max(t_lo, t)
+            if nnz < k2:
+                k2, thres2, set2 = nnz, t, True
+        if t_hi is None:
+            t = 2.0 * t          # too many selected: double
+        elif t_lo is None:
+            t = t / 2.0          # too few selected: halve
+        else:
+            t = t_lo + (t_hi - t_lo) / 2.0
+    in1 = a64 >= thres1 if k1 > 0 else np.zeros(d, dtype=bool)
+    in2 = (~in1) & (a64 >= thres2)
+    iota1 = np.nonzero(in1)[0]
+    iota2 = np.nonzero(in2)[0]
+    need = k - k1
+    R = len(iota2) - need + 1
+    if R < 1:
+        raise AssertionError("window range R < 1 — impossible under readings Q8/Q9")
+    rand = 0 if rand_mode == RAND_FIRST else (window_hash(seed, step, rank, 0) * R) >> 64
+    iota = np.sort(np.concatenate([iota1, iota2[rand:rand + need]])).astype(np.uint32)
+    kappa = x[iota.astype(np.int64)].copy()
+    key1 = ceil_f32_bits(thres1) if set1 else F32_INF_BITS
+    key2 = ceil_f32_bits(thres2) if set2 else 0
+    return MSTopKResult(idx=iota, val=kappa, mean=abar, u=u, k=k, k1=k1, k2=k2, thres1=thres1,
+                        thres2=thres2, thres1_set=set1, thres2_set=set2, key1=key1, key2=key2,
+                        len2=int(len(iota2)), rand=int(rand), trials=trials)
