@@ -30,22 +30,26 @@ def _run(P, tmp_path, **kw):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs, box has {torch.cuda.device_count()}")
     out = tmp_path / "res.json"
-    args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
-            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
-            "--out", str(out)]
+    extra = []
     for key, v in kw.items():
         if v is True:
-            args.append("--" + key.replace("_", "-"))
+            extra.append("--" + key.replace("_", "-"))
         else:
-            args += ["--" + key.replace("_", "-"), str(v)]
-    proc = subprocess.Popen(args, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=ROOT,
-                            start_new_session=True)
-    try:
-        so, se = proc.communicate(timeout=150)
-    except subprocess.TimeoutExpired:
-        os.killpg(proc.pid, 9)  # the whole torchrun process group, workers included
-        so, se = proc.communicate()
-        pytest.fail("multi-GPU worker timed out:\n" + so[-2000:] + se[-3000:])
+            extra += ["--" + key.replace("_", "-"), str(v)]
+    for attempt in range(3):  # the free port can be taken between probe and bind: retry on EADDRINUSE
+        args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+                "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
+                "--out", str(out)] + extra
+        proc = subprocess.Popen(args, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=ROOT,
+                                start_new_session=True)
+        try:
+            so, se = proc.communicate(timeout=150)
+        except subprocess.TimeoutExpired:
+            os.killpg(proc.pid, 9)  # the whole torchrun process group, workers included
+            so, se = proc.communicate()
+            pytest.fail("multi-GPU worker timed out:\n" + so[-2000:] + se[-3000:])
+        if proc.returncode == 0 or "EADDRINUSE" not in se:
+            break
     assert proc.returncode == 0, so[-3000:] + se[-3000:]
     verdict = json.loads(out.read_text())
     assert verdict["ok"], json.dumps(verdict["steps"], indent=1)[:4000]
