@@ -406,6 +406,23 @@ def main():
                "h2d_bytes_per_step": 4 * a.d, "d2h_bytes_per_step": 4 * chunks * ctx.chunk_words,
                "api": "tk_step_host (pinned host gradient in, gathered (index, value) pairs out; residual device-resident)"}
 
+    # MSTopK's recall against the exact top-k of Eq. 2 (the comparison of the paper's Fig. 6), both
+    # selections made by libtk's kernels on the same step-0 gradient (no error feedback), outside
+    # the timed region: |iota_MSTopK ∩ iota_exact| / k and the ratio of the selected |x| mass
+    recall = None
+    if rank == 0 and P == 1 and n == 1 and a.select == "mstopk" and not a.ncu:
+        sel = {}
+        for kind in ("mstopk", "exact"):
+            c = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, seed=2010_10458, select=kind, error_feedback=False,
+                           device=local)
+            idx, val = c.compress(gs[0])
+            torch.cuda.synchronize()
+            sel[kind] = (idx.long(), val.abs().double().sum().item())
+            c.close()
+        hit = int(torch.isin(sel["mstopk"][0], sel["exact"][0]).sum().item())
+        recall = {"index_recall": hit / k, "magnitude_ratio": sel["mstopk"][1] / sel["exact"][1],
+                  "note": "MSTopK vs exact top-k (Eq. 2) on the step-0 gradient, both on the GPU, EF off"}
+
     cpu = None
     if rank == 0 and P == 1 and not a.no_cpu_baseline and not a.ncu:
         cpu = cpu_baseline(a, P)
@@ -424,7 +441,7 @@ def main():
                            "l2": "inputs larger than L2: each step reads a fresh g (4d B) and touches r and out: "
                                  f"{12 * a.d / 1e6:.0f} MB per rank per step vs 126 MB L2; no explicit flush"},
                 "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": e2e, "stages": stages}
+                "e2e": e2e, "stages": stages, "recall_vs_exact": recall}
         emit(line)
     ctx.close()
     if ws > 1:
