@@ -103,3 +103,11 @@ def test_bucket_step_sgd_updates_the_layer_views():
     with pytest.raises(ValueError):
         b.views(torch.zeros(b.d + 1, device="cuda"))
     b.close()
+
+
+def test_bucket_has_no_cpu_fallback():
+    if torch.cuda.is_available():
+        pytest.skip("checks the CPU-only failure mode")
+    tk = _tk()
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        tk.Bucket(SHAPES)
