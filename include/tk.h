@@ -12,6 +12,7 @@
  *   HiTopKComm (m x n virtual nodes), Algorithm 2    — P:203-248
  * and the adjacent rows of SURVEY.md §8(f):
  *   exact top-k selector (TK_SELECT_EXACT)           — Eq. 2, P:131-139 (F1)
+ *   MSTopK with the prose threshold search           — P:148, reading Q33 (F3, TK_SELECT_PROSE)
  *   fused all-gather pushed over NVLink (TK_AG_PUSH) — P:197 (F2)
  *   FP16 values on the wire (TK_WIRE_F16)            — Fig. 7 ran FP16, P:337 (F3)
  *   SGD update fused into decompression (tk_step_sgd)— Eq. 1, P:65-67 (F4)
@@ -54,7 +55,10 @@ typedef enum tk_status {
   TK_ERR_CUDA = 5,        /* CUDA runtime error; text in tk_last_error                        */
   TK_ERR_NCCL = 6,        /* NCCL error; text in tk_last_error                                 */
   TK_ERR_STATE = 7,       /* wrong call order (e.g. tk_sparse_allgather with P == 1 comm absent)*/
-  TK_ERR_NOMEM = 8        /* device allocation of scratch failed                              */
+  TK_ERR_NOMEM = 8,       /* device allocation of scratch failed                              */
+  TK_ERR_TIMEOUT = 9      /* the fused all-gather waited longer than push_timeout_ms for a peer's
+                             packets (a peer died or stalled): that step's aggregate is invalid;
+                             sticky, reported by the next tk_get_stats                          */
 } tk_status;
 
 enum { TK_RAND_SEEDED = 0, TK_RAND_FIRST = 1 };   /* Alg. 1 l.27 window start (Q10)           */
@@ -63,11 +67,16 @@ enum { TK_AG_PUSH = 0, TK_AG_NCCL = 1 };          /* flat sparse all-gather (A9)
                                                      PUSH = the compression writes its pairs into
                                                      every peer's buffer over NVLink (P <= 8);
                                                      NCCL = ncclAllGather after the compression */
-enum { TK_SELECT_MSTOPK = 0, TK_SELECT_EXACT = 1 }; /* selector:
+enum { TK_SELECT_MSTOPK = 0, TK_SELECT_EXACT = 1, TK_SELECT_PROSE = 2 };
+                                                  /* selector:
                                                      MSTOPK = Alg. 1 under Q1-Q27;
                                                      EXACT = exact top-k of Eq. 2:
                                                      the k largest |acc|, ties -> lower index (Q6);
-                                                     n_iters is then unused                     */
+                                                     n_iters is then unused;
+                                                     PROSE = MSTopK with the threshold search of
+                                                     the prose of P:148 (start at a-bar, double /
+                                                     halve until bracketed, then bisect the
+                                                     bracket; reading Q33); selection as Alg. 1 */
 enum { TK_WIRE_F32 = 0, TK_WIRE_F16 = 1 };         /* value format on the wire (Fig. 7
                                                      ran FP16; reading Q31): F16 = each
                                                      selected value v is sent as
@@ -103,7 +112,29 @@ typedef struct tk_config {
   uint32_t ag_mode;        /* flat all-gather mode (TK_AG_PUSH or TK_AG_NCCL)                  */
   uint32_t select;         /* TK_SELECT_MSTOPK (default) or TK_SELECT_EXACT                    */
   uint32_t wire;           /* TK_WIRE_F32 (default) or TK_WIRE_F16 (values sent as binary16)  */
+  /* --- execution options (0 = default everywhere; none changes a result bit) --------------- */
+  uint32_t exact_trial_counts; /* 1: every trial's nnz in tk_stats is the exact count (Alg. 1
+                              l.10).  Default 0: a trial whose threshold lies below the key
+                              the previous call predicted is only known to have nnz > k (the
+                              decision it needs), its nnz is reported as TK_NNZ_NOT_COUNTED;
+                              1 adds a whole-vector count pass (4d bytes) when that happens */
+  uint32_t disable_ef_compaction; /* 1: never compact in the error-feedback pass (the whole-vector
+                              first pass runs every call).  Default 0                            */
+  uint32_t first_pass_keys;  /* keys counted by a whole-vector first pass along the predicted
+                              path, 1..3 (0 = 3)                                                */
+  uint32_t check_selection;  /* 1: verify every selection on the device (strictly ascending,
+                              in range; a violation traps); debugging only                       */
+  uint32_t push_timeout_ms;  /* TK_AG_PUSH: how long a decompression waits for one peer packet
+                              before it gives up and reports TK_ERR_TIMEOUT (0 = 300000, 5 min;
+                              ranks may legitimately drift by seconds: checkpoints, eval)         */
+  uint32_t loopback;         /* 1: emulate rank `rank` of `nranks` on this GPU without any
+                              communicator (uid may be NULL): only tk_compress,
+                              tk_compress_segment, tk_decompress and the tk_loopback_* calls are
+                              allowed; tk_step / tk_sparse_allgather return TK_ERR_STATE.  For
+                              single-GPU parity tests of the multi-GPU kernels                   */
 } tk_config;
+
+#define TK_NNZ_NOT_COUNTED 0xFFFFFFFFu
 
 /* Snapshot of the last compression's MSTopK control block (for parity checks). */
 typedef struct tk_stats {
@@ -131,9 +162,10 @@ typedef struct tk_stats {
                               end of selection                                                 */
   uint32_t ef_compacted;   /* 1 if the entries were compacted inside the EF pass at the key the
                               previous call predicted (no whole-vector count pass ran)         */
-  uint64_t nnz_lower_bound;/* bit i set: trial i's threshold lay below that compaction key, so
-                              nnz[i] is a lower bound of the count, and > k (the decision and
-                              every result are exact)                           */
+  uint64_t nnz_not_counted;/* bit i set: trial i's threshold lay below that compaction key; its
+                              count is only known to exceed k (the decision it needs; every
+                              result is exact) and nnz[i] = TK_NNZ_NOT_COUNTED.
+                              Always 0 with exact_trial_counts = 1                             */
 } tk_stats;
 
 /* k = max(1, floor(rho * d)) in fp64 (Q13).  Host-only, pure.  0 on invalid input. */
@@ -154,6 +186,18 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
  *   val [k]  out    kappa = acc[iota], bit-copied (Q12); TK_WIRE_F16: the fp16-rounded values sent
  * g must not alias r, idx or val. */
 tk_status tk_compress(tk_ctx* ctx, const float* g, float* r, uint32_t* idx, float* val);
+
+/* Segment compression, HiTopKComm steps 1-2 for one GPU (Eq. 4-5; Alg. 2 l.2-8):
+ * MSTopK (or the configured selector) of acc = (sum_{q=0..nsrc-1} src[q]) (+ r with error
+ * feedback), the sum taken in ascending q, left to right, fp32 round-to-nearest (reading Q20).
+ *   src  host array of nsrc DEVICE pointers, each to L = seg_len floats (tk_query), 16-byte
+ *        aligned, readable from this GPU (local buffers or CUDA-IPC-mapped peer memory)
+ *   nsrc 1, 2, 4 or 8 (nsrc = 1: acc = src[0] (+ r), i.e. tk_compress on a length-L vector)
+ *   r    [L] in/out residual (error feedback; ignored otherwise); idx/val [k~] out as tk_compress
+ * Valid in every mode: in HiTopKComm mode it is the step-1+2 kernel tk_step runs (there with the
+ * row peers' buffers), in flat mode L = d.  Does not advance the step counter. */
+tk_status tk_compress_segment(tk_ctx* ctx, const float* const* src, uint32_t nsrc, float* r, uint32_t* idx,
+                              float* val);
 
 /* Sparse All-Gather: gathered [P][cw] u32, rank-major, each rank's chunk laid out as
  * [idx k | bits(val) k] (Q15, cw = 2k) or, with TK_WIRE_F16, [idx k | binary16 val k] padded to
@@ -198,6 +242,23 @@ tk_status tk_step_host(tk_ctx* ctx, const float* g_host, uint32_t* gathered_host
  * A caller that writes its gradient here and passes this pointer as g to tk_step avoids the
  * copy-in (tk_step copies any other g into it first).  NULL for flat mode. */
 tk_status tk_input_buffer(tk_ctx* ctx, float** g);
+
+/* --- loopback (cfg.loopback = 1): single-GPU emulation of the fused all-gather ----
+ * TEST INFRASTRUCTURE for the multi-GPU kernels on one GPU.  A tagged packet is 16 bytes: {u64
+ * idx | tag << 32, u64 bits(val) | tag << 32}; a rank's chunk is k packets.
+ * tk_loopback_push: tk_compress of this rank, which also writes its k pairs as packets tagged
+ *   `tag` (!= 0) to slots[q] for q < nslots (host array of device pointers to k-packet slots,
+ *   e.g. this rank's chunk in every emulated rank's packet buffer) - the same kernel and stores
+ *   tk_step uses with TK_AG_PUSH, there with CUDA-IPC peer pointers.  chunk [cw] receives the
+ *   plain packed pairs.
+ * tk_loopback_decompress: the rank-ordered decompression of nchunks k-packet chunks (packets
+ *   [nchunks][k]) that waits, per packet, for `tag` (up to push_timeout_ms, then TK_ERR_TIMEOUT
+ *   at the next tk_get_stats); out [d] (flat) or [d/n] receives the aggregate and plain_out
+ *   (optional, [nchunks][cw]) the consumed pairs in the plain layout. */
+tk_status tk_loopback_push(tk_ctx* ctx, const float* g, float* r, uint32_t* chunk, void* const* slots,
+                           uint32_t nslots, uint32_t tag);
+tk_status tk_loopback_decompress(tk_ctx* ctx, const void* packets, uint32_t nchunks, uint32_t tag, float* out,
+                                 uint32_t* plain_out);
 
 /* Copy the control block of the last compression to *st (synchronises the stream). */
 tk_status tk_get_stats(tk_ctx* ctx, tk_stats* st);

@@ -23,7 +23,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libtk.so")
 
 STATUS = {0: "TK_OK", 1: "TK_ERR_INVALID_ARG", 2: "TK_ERR_RANGE", 3: "TK_ERR_CONFIG", 4: "TK_ERR_NONFINITE",
-          5: "TK_ERR_CUDA", 6: "TK_ERR_NCCL", 7: "TK_ERR_STATE", 8: "TK_ERR_NOMEM"}
+          5: "TK_ERR_CUDA", 6: "TK_ERR_NCCL", 7: "TK_ERR_STATE", 8: "TK_ERR_NOMEM", 9: "TK_ERR_TIMEOUT"}
+NNZ_NOT_COUNTED = 0xFFFFFFFF  # tk_stats.nnz of a trial whose count was not taken (only "nnz > k" is known)
 NMAX = 52
 
 
@@ -39,7 +40,10 @@ class _Config(ctypes.Structure):
                 ("group_size", ctypes.c_uint32), ("seed", ctypes.c_uint64), ("rand_mode", ctypes.c_uint32),
                 ("error_feedback", ctypes.c_uint32), ("step4", ctypes.c_uint32),
                 ("levels_per_pass", ctypes.c_uint32), ("device", ctypes.c_int32), ("rs_mode", ctypes.c_uint32),
-                ("ag_mode", ctypes.c_uint32), ("select", ctypes.c_uint32), ("wire", ctypes.c_uint32)]
+                ("ag_mode", ctypes.c_uint32), ("select", ctypes.c_uint32), ("wire", ctypes.c_uint32),
+                ("exact_trial_counts", ctypes.c_uint32), ("disable_ef_compaction", ctypes.c_uint32),
+                ("first_pass_keys", ctypes.c_uint32), ("check_selection", ctypes.c_uint32),
+                ("push_timeout_ms", ctypes.c_uint32), ("loopback", ctypes.c_uint32)]
 
 
 class _Stats(ctypes.Structure):
@@ -54,14 +58,15 @@ class _Stats(ctypes.Structure):
                 ("nonfinite", ctypes.c_uint32), ("compacted", ctypes.c_uint32), ("n_compacted", ctypes.c_uint32),
                 ("n_phases", ctypes.c_uint32),
                 ("phase_ns", ctypes.c_uint64 * 12), ("ef_compacted", ctypes.c_uint32),
-                ("nnz_lower_bound", ctypes.c_uint64)]
+                ("nnz_not_counted", ctypes.c_uint64)]
 
 
 # Every symbol include/tk.h declares (checked by tests/test_abi.py).
 EXPORTS = ["tk_k", "tk_get_unique_id", "tk_init", "tk_compress", "tk_sparse_allgather", "tk_decompress",
            "tk_step", "tk_step_host", "tk_get_stats", "tk_set_step", "tk_query", "tk_launch_count",
            "tk_destroy", "tk_status_string", "tk_last_error", "tk_profile_begin", "tk_profile_end",
-           "tk_stage_name", "tk_input_buffer", "tk_step_sgd"]
+           "tk_stage_name", "tk_input_buffer", "tk_step_sgd", "tk_compress_segment", "tk_loopback_push",
+           "tk_loopback_decompress"]
 NSTAGES = 16
 
 
@@ -93,6 +98,9 @@ def _load():
         "tk_profile_end": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(U32)]),
         "tk_stage_name": (ctypes.c_char_p, [U32]),
         "tk_input_buffer": (I32, [P, ctypes.POINTER(P)]),
+        "tk_compress_segment": (I32, [P, ctypes.POINTER(P), U32, P, P, P]),
+        "tk_loopback_push": (I32, [P, P, P, P, ctypes.POINTER(P), U32, U32]),
+        "tk_loopback_decompress": (I32, [P, P, U32, U32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -140,17 +148,23 @@ def broadcast_unique_id(group=None) -> bytes:
     return bytes(t.tolist())
 
 
-def _ptr(t, name, dtype):
+def _ptr(t, name, dtype, numel=None, device=None):
+    """Device pointer of a tensor, after checking what the C ABI cannot (it takes no lengths):
+    type, device (the context's GPU), contiguity and - when given - at least `numel` elements."""
     if t is None:
         return None
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch tensor")
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (libtk has no CPU path)")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, the context on {device}")
     if t.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name} has {t.numel()} elements, needs {numel}")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -176,7 +190,8 @@ class Stats:
     n_compacted: int
     phase_us: list  # k_compress phase durations (device globaltimer, CTA 0)
     ef_compacted: bool  # the entries came from the EF pass (predicted key), no whole-vector count pass
-    nnz_lower_bound: int  # bit i: trials[i]'s nnz is a lower bound (> k) - its threshold lay below that key
+    nnz_not_counted: int  # bit i: trials[i]'s count was not taken (its threshold lay below that key;
+                          # only nnz > k is known) and trials[i][3] == NNZ_NOT_COUNTED
 
 
 class _DeviceView:
@@ -195,14 +210,21 @@ class _DeviceView:
 class Context:
     """One rank's libtk context (tk_init).  ``d, rho, n_iters`` follow the paper's statement of
     the problem (x in R^d, k = rho*d, N samplings, P workers, m x n for HiTopKComm).
-    ``select="exact"`` replaces MSTopK by the exact top-k of Eq. 2 (ties -> lower index);
-    ``wire="f16"`` sends the values as binary16 (Fig. 7's FP16, reading Q31)."""
+    ``select="exact"`` replaces MSTopK by the exact top-k of Eq. 2 (ties -> lower index),
+    ``select="prose"`` runs MSTopK with the prose's halve/double threshold search (P:148, Q33);
+    ``wire="f16"`` sends the values as binary16 (Fig. 7's FP16, reading Q31).
+    Execution options (none changes a result bit): ``exact_trial_counts`` (count every trial
+    exactly, for parity logs), ``ef_compaction``, ``first_pass_keys``, ``check_selection``,
+    ``push_timeout_ms``; ``loopback=True`` emulates rank ``rank`` of ``nranks`` on this GPU
+    without communicators (single-GPU tests of the multi-GPU kernels)."""
 
     def __init__(self, d: int, rho: float = 0.001, n_iters: int = 10, *, k: int = 0, nranks: int = 1, rank: int = 0,
                  group_size: int = 1, seed: int = 0, rand_mode: str = "seeded", error_feedback: bool = True,
                  step4: str = "dense", levels_per_pass: int = 0, device: int | None = None, uid: bytes | None = None,
                  stream: torch.cuda.Stream | None = None, rs_mode: str = "ordered", ag_mode: str = "push",
-                 select: str = "mstopk", wire: str = "f32"):
+                 select: str = "mstopk", wire: str = "f32", exact_trial_counts: bool = False,
+                 ef_compaction: bool = True, first_pass_keys: int = 0, check_selection: bool = False,
+                 push_timeout_ms: int = 0, loopback: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("libtk needs a CUDA device (B200, sm_100a); there is no CPU fallback")
         dev = torch.cuda.current_device() if device is None else int(device)
@@ -213,9 +235,13 @@ class Context:
                       rand_mode={"seeded": 0, "first": 1}[rand_mode], error_feedback=1 if error_feedback else 0,
                       step4={"dense": 0, "sparse": 1}[step4], levels_per_pass=int(levels_per_pass), device=dev,
                       rs_mode={"ordered": 0, "nccl": 1}[rs_mode], ag_mode={"push": 0, "nccl": 1}[ag_mode],
-                      select={"mstopk": 0, "exact": 1}[select], wire={"f32": 0, "f16": 1}[wire])
+                      select={"mstopk": 0, "exact": 1, "prose": 2}[select], wire={"f32": 0, "f16": 1}[wire],
+                      exact_trial_counts=1 if exact_trial_counts else 0,
+                      disable_ef_compaction=0 if ef_compaction else 1, first_pass_keys=int(first_pass_keys),
+                      check_selection=1 if check_selection else 0, push_timeout_ms=int(push_timeout_ms),
+                      loopback=1 if loopback else 0)
         self._ctx = ctypes.c_void_p()
-        if nranks > 1 and uid is None:
+        if nranks > 1 and uid is None and not loopback:
             raise ValueError("nranks > 1 needs the NCCL unique id (broadcast_unique_id())")
         st = _lib.tk_init(ctypes.byref(cfg), uid, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(self._ctx))
         if st != 0:
@@ -227,6 +253,7 @@ class Context:
         self.nranks, self.m, self.n, self.rank = P.value, m.value, n.value, int(rank)
         self.error_feedback = bool(error_feedback)
         self.wire = wire
+        self.select = select
         # u32 words of one packed chunk: [idx k | fp32 val k] or [idx k | binary16 val k (padded)]
         self.chunk_words = 2 * self.k if wire == "f32" else self.k + (self.k + 1) // 2
 
@@ -238,62 +265,117 @@ class Context:
     def _empty(self, n, dtype):
         return torch.empty(n, dtype=dtype, device=self.device)
 
+    def _p(self, t, name, dtype, numel=None):
+        return _ptr(t, name, dtype, numel, self.device)
+
     @property
     def chunks(self) -> int:
         return self.nranks if self.n == 1 else self.m
+
+    @property
+    def out_len(self) -> int:
+        """Length of a decompression output: d (flat) or the segment d/n (HiTopKComm)."""
+        return self.d if self.n == 1 else self.seg_len
 
     def compress(self, g, r=None, idx=None, val=None):
         """tk_compress: returns (idx uint32-as-int32 tensor, val float32 tensor)."""
         idx = self._empty(self.k, torch.int32) if idx is None else idx
         val = self._empty(self.k, torch.float32) if val is None else val
-        self._check(_lib.tk_compress(self._ctx, _ptr(g, "g", torch.float32),
-                                     _ptr(r, "r", torch.float32) if self.error_feedback else None,
-                                     _ptr(idx, "idx", torch.int32), _ptr(val, "val", torch.float32)))
+        self._check(_lib.tk_compress(self._ctx, self._p(g, "g", torch.float32, self.d),
+                                     self._p(r, "r", torch.float32, self.d) if self.error_feedback else None,
+                                     self._p(idx, "idx", torch.int32, self.k), self._p(val, "val", torch.float32, self.k)))
+        return idx, val
+
+    def compress_segment(self, srcs, r=None, idx=None, val=None):
+        """tk_compress_segment: MSTopK of the ordered sum of the source segments (HiTopKComm steps
+        1-2, Eq. 4-5) (+ r with error feedback); srcs = 1, 2, 4 or 8 CUDA tensors of seg_len
+        floats (local, or views of peer memory).  Returns (idx, val) of k~ pairs."""
+        srcs = list(srcs)
+        idx = self._empty(self.k, torch.int32) if idx is None else idx
+        val = self._empty(self.k, torch.float32) if val is None else val
+        arr = (ctypes.c_void_p * len(srcs))(*[self._p(t, f"src[{i}]", torch.float32, self.seg_len).value
+                                               for i, t in enumerate(srcs)])
+        self._check(_lib.tk_compress_segment(self._ctx, arr, len(srcs),
+                                             self._p(r, "r", torch.float32, self.seg_len) if self.error_feedback else None,
+                                             self._p(idx, "idx", torch.int32, self.k),
+                                             self._p(val, "val", torch.float32, self.k)))
         return idx, val
 
     def sparse_allgather(self, idx, val, gathered=None):
         gathered = self._empty(self.chunks * self.chunk_words, torch.int32) if gathered is None else gathered
-        self._check(_lib.tk_sparse_allgather(self._ctx, _ptr(idx, "idx", torch.int32), _ptr(val, "val", torch.float32),
-                                             _ptr(gathered, "gathered", torch.int32)))
+        self._check(_lib.tk_sparse_allgather(self._ctx, self._p(idx, "idx", torch.int32, self.k),
+                                             self._p(val, "val", torch.float32, self.k),
+                                             self._p(gathered, "gathered", torch.int32, self.chunks * self.chunk_words)))
         return gathered
 
     def decompress(self, gathered, nchunks=None, out=None):
-        n_out = self.d if self.n == 1 else self.seg_len
-        out = self._empty(n_out, torch.float32) if out is None else out
+        out = self._empty(self.out_len, torch.float32) if out is None else out
         nch = self.chunks if nchunks is None else int(nchunks)
-        self._check(_lib.tk_decompress(self._ctx, _ptr(gathered, "gathered", torch.int32), nch,
-                                       _ptr(out, "out", torch.float32)))
+        self._check(_lib.tk_decompress(self._ctx, self._p(gathered, "gathered", torch.int32, nch * self.chunk_words),
+                                       nch, self._p(out, "out", torch.float32, self.out_len)))
         return out
 
     def step(self, g, r=None, out=None, gathered=None):
         """tk_step: one whole iteration; returns the dense aggregated gradient."""
         out = self._empty(self.d, torch.float32) if out is None else out
-        self._check(_lib.tk_step(self._ctx, _ptr(g, "g", torch.float32),
-                                 _ptr(r, "r", torch.float32) if self.error_feedback else None,
-                                 _ptr(out, "out", torch.float32),
-                                 _ptr(gathered, "gathered", torch.int32) if gathered is not None else None))
+        self._check(_lib.tk_step(self._ctx, self._p(g, "g", torch.float32, self.d),
+                                 self._p(r, "r", torch.float32, self.seg_len) if self.error_feedback else None,
+                                 self._p(out, "out", torch.float32, self.d),
+                                 self._p(gathered, "gathered", torch.int32, self.chunks * self.chunk_words)
+                                 if gathered is not None else None))
         return out
 
     def step_sgd(self, g, r, w, lr: float, out=None, gathered=None):
         """tk_step_sgd: one iteration plus Eq. 1's update w -= lr * aggregate, fused into the
         decompression; w is updated in place (out optional)."""
-        self._check(_lib.tk_step_sgd(self._ctx, _ptr(g, "g", torch.float32),
-                                     _ptr(r, "r", torch.float32) if self.error_feedback else None,
-                                     _ptr(w, "w", torch.float32), ctypes.c_float(lr),
-                                     _ptr(out, "out", torch.float32) if out is not None else None,
-                                     _ptr(gathered, "gathered", torch.int32) if gathered is not None else None))
+        self._check(_lib.tk_step_sgd(self._ctx, self._p(g, "g", torch.float32, self.d),
+                                     self._p(r, "r", torch.float32, self.seg_len) if self.error_feedback else None,
+                                     self._p(w, "w", torch.float32, self.d), ctypes.c_float(lr),
+                                     self._p(out, "out", torch.float32, self.d) if out is not None else None,
+                                     self._p(gathered, "gathered", torch.int32, self.chunks * self.chunk_words)
+                                     if gathered is not None else None))
         return w
+
+    # loopback (single-GPU emulation of the fused all-gather, tk_loopback_*): a k-packet chunk is
+    # k x 16 bytes, held here as int64 tensors of 2k words
+    def loopback_push(self, g, r, chunk, slots, tag: int):
+        """tk_loopback_push: compress (into the plain packed `chunk`) and write this rank's pairs as
+        packets tagged `tag` to every slot (int64 tensors of >= 2k elements)."""
+        slots = list(slots)
+        arr = (ctypes.c_void_p * len(slots))(*[self._p(t, f"slot[{i}]", torch.int64, 2 * self.k).value
+                                               for i, t in enumerate(slots)])
+        self._check(_lib.tk_loopback_push(self._ctx, self._p(g, "g", torch.float32, self.d),
+                                          self._p(r, "r", torch.float32, self.d) if self.error_feedback else None,
+                                          self._p(chunk, "chunk", torch.int32, self.chunk_words), arr, len(slots),
+                                          int(tag)))
+
+    def loopback_decompress(self, packets, nchunks: int, tag: int, out=None, plain_out=None):
+        """tk_loopback_decompress: rank-ordered decompression of nchunks packet chunks that waits for
+        `tag` in every packet; returns out (and fills plain_out, [nchunks][chunk_words], if given)."""
+        out = self._empty(self.out_len, torch.float32) if out is None else out
+        self._check(_lib.tk_loopback_decompress(
+            self._ctx, self._p(packets, "packets", torch.int64, 2 * self.k * nchunks), int(nchunks), int(tag),
+            self._p(out, "out", torch.float32, self.out_len),
+            self._p(plain_out, "plain_out", torch.int32, nchunks * self.chunk_words) if plain_out is not None else None))
+        return out
 
     def step_host(self, g_host, gathered_host=None, out_host=None):
         """tk_step_host: HOST buffers in/out (numpy or pinned CPU tensors); synchronous."""
-        def hp(a):
+        def hp(a, n, name):
             if a is None:
                 return None
             if isinstance(a, torch.Tensor):
-                assert not a.is_cuda and a.is_contiguous()
+                if a.is_cuda or not a.is_contiguous():
+                    raise ValueError(f"{name} must be a contiguous host tensor")
+                if a.numel() * a.element_size() < 4 * n:
+                    raise ValueError(f"{name} holds fewer than {n} 4-byte words")
                 return ctypes.c_void_p(a.data_ptr())
+            if not a.flags["C_CONTIGUOUS"] or a.nbytes < 4 * n:
+                raise ValueError(f"{name} must be contiguous with >= {n} 4-byte words")
             return ctypes.c_void_p(a.ctypes.data)
-        self._check(_lib.tk_step_host(self._ctx, hp(g_host), hp(gathered_host), hp(out_host)))
+        self._check(_lib.tk_step_host(self._ctx, hp(g_host, self.d, "g_host"),
+                                      hp(gathered_host, self.chunks * self.chunk_words, "gathered_host"),
+                                      hp(out_host, self.d, "out_host")))
         return gathered_host, out_host
 
     def stats(self) -> Stats:
@@ -307,7 +389,7 @@ class Context:
                      key2=s.key2, len2=s.len2, rand=s.rand_start, step=s.step, nonfinite=bool(s.nonfinite),
                      compacted=bool(s.compacted), n_compacted=int(s.n_compacted),
                      phase_us=[(s.phase_ns[i + 1] - s.phase_ns[i]) / 1e3 for i in range(max(0, s.n_phases - 1))],
-                     ef_compacted=bool(s.ef_compacted), nnz_lower_bound=int(s.nnz_lower_bound))
+                     ef_compacted=bool(s.ef_compacted), nnz_not_counted=int(s.nnz_not_counted))
 
     def input_buffer(self):
         """HiTopKComm ordered mode: a torch view of libtk's peer-visible gradient buffer (write the

@@ -43,7 +43,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if not force and os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in deps):
         return OUT
     inc, lib = nccl_dirs()
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC,-O2",
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false", "--split-compile=0", "-Xcompiler", "-fPIC,-O2",
            "-shared", "-o", OUT, *srcs, "-I", os.path.join(ROOT, "include"), "-I", inc, "-L", lib,
            "-l:libnccl.so.2", f"-Xlinker=-rpath,{lib}", "-lcudart"]
     if verbose:

@@ -39,9 +39,12 @@ struct tk_ctx {
   uint64_t S = 0;                     // slab length
   uint32_t occ_dec = 1;               // resident decompression CTAs per SM
   uint32_t levels = 4, npass = 0;
-  uint32_t debug_check = 0;           // TK_CHECK=1: verify every selection (ascending, in range) on the device
-  uint32_t ef_compact = 1;
-  uint32_t ef_compact_peers = 0;      // TK_EF_COMPACT_PEERS=1: also with NP > 0 (open issue)            // compaction in the ef phase (TK_EF_COMPACT=0 disables; bits unchanged)
+  uint32_t debug_check = 0;           // cfg.check_selection: verify every selection on the device
+  uint32_t ef_compact = 1;            // compaction in the ef phase (cfg.disable_ef_compaction; bits unchanged)
+  uint32_t seq = 0;                   // k_compress launch sequence number (overflow flags, never 0)
+  uint32_t* dev_err = nullptr;        // device word: the fused all-gather's wait timed out (sticky)
+  uint32_t timeout_sticky = 0;
+  uint64_t timeout_ns = 0;
   int lev_sched[NMAX];
   uint32_t units_per_warp = 1;        // ef phase: aligned power-of-two run of 512-element units per warp
   uint32_t* cta_cls = nullptr;        // [4][grid] per-CTA class counts, entries
@@ -142,6 +145,7 @@ SearchParams search_params(const tk_ctx* c) {
 
 template <int SEL>
 const void* compress_kernel_sel(bool ef, int np) {
+  // NP: the number of gradient sources summed in the ef phase (0 = one plain vector)
   switch ((ef ? 100 : 0) + np) {
     case 100: return reinterpret_cast<const void*>(&k_compress<true, 0, SEL>);
     case 102: return reinterpret_cast<const void*>(&k_compress<true, 2, SEL>);
@@ -156,10 +160,11 @@ const void* compress_kernel_sel(bool ef, int np) {
 }
 
 const void* compress_kernel(bool ef, int np, uint32_t sel) {
-  return sel == TK_SELECT_EXACT ? compress_kernel_sel<SEL_EXACT>(ef, np) : compress_kernel_sel<SEL_MSTOPK>(ef, np);
+  if (sel == TK_SELECT_EXACT) return compress_kernel_sel<SEL_EXACT>(ef, np);
+  if (sel == TK_SELECT_PROSE) return compress_kernel_sel<SEL_PROSE>(ef, np);
+  return compress_kernel_sel<SEL_MSTOPK>(ef, np);
 }
 
-int peer_sources(const tk_ctx* c) { return (c->n > 1 && c->cfg.rs_mode == TK_RS_ORDERED) ? (int)c->n : 0; }
 
 // MSTopK on a vector of length L (= c->L) with error feedback: g (+ r) -> idx/val, as ONE
 // cooperative launch of k_compress.  With peers != nullptr the gradient is the ordered sum of the
@@ -173,7 +178,13 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.g = g;
   if (peers) f.pr = *peers;
   f.r = ef ? r : nullptr;
-  f.acc = ef ? r : g;
+  // acc lives in r (EF, in place), in the segment scratch (peer sum without EF) or is g itself
+  f.accw = ef ? r : (np > 0 ? c->seg : nullptr);
+  if (np > 0 && !ef && !c->seg) return fail(c, TK_ERR_STATE, "no scratch segment for the peer sum");
+  f.acc = f.accw ? f.accw : g;
+  if (++c->seq == 0) c->seq = 1;  // overflow flags hold the launch that raised them (0 = never)
+  f.seq = c->seq;
+  f.exact_counts = c->cfg.exact_trial_counts ? 1u : 0u;
   f.units_per_warp = c->units_per_warp;
   f.cta_sum = c->cta_sum;
   f.cta_max = c->cta_max;
@@ -195,16 +206,14 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.lev0 = c->lev_sched[0];
   f.cap_levels = (int)c->levels;
   f.max_pass = (int)c->npass;
-  // EF-pass compaction is off when the EF pass sums peer segments (HiTopKComm ordered
-  // reduce-scatter): with it on, 1 in ~6 4-GPU bench runs hit an illegal address that no device
-  // check, launch-blocking or sanitised run reproduces (open issues)
-  f.ef_compact = (np == 0 || c->ef_compact_peers) ? c->ef_compact : 0u;
+  f.ef_compact = c->ef_compact;
   const void* kern = compress_kernel(ef, np, c->cfg.select);
   if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
   void* args[] = {&f};
   TK_CUDA(c, cudaLaunchCooperativeKernel(kern, dim3(c->grid), dim3(THREADS), args, 0, c->stream));
   if (c->debug_check) {
     k_check_sel<<<1, 1024, 0, c->stream>>>(idx, c->k, c->L, (uint32_t)c->rank, (uint32_t)c->step, 0u);
+    TK_TRY(check_launch(c, "k_check_sel"));
   }
   TK_TRY(check_launch(c, "k_compress"));
   mark(c, TK_STAGE_COMPRESS);
@@ -266,10 +275,14 @@ tk_status plan_launches(tk_ctx* c) {
   int v = 0;
   TK_CUDA(c, cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, c->device));
   c->sms = (uint32_t)v;
-  int occ = 0, o7 = 0;
-  const void* kern = compress_kernel(c->cfg.error_feedback != 0, peer_sources(c), c->cfg.select);
-  if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count");
-  TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, 0));
+  int occ = 1 << 30, o7 = 0;
+  for (int np : {0, 2, 4, 8}) {  // every source count tk_compress_segment may launch
+    const void* kern = compress_kernel(c->cfg.error_feedback != 0, np, c->cfg.select);
+    if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count");
+    int o = 0;
+    TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, THREADS, 0));
+    occ = std::min(occ, o);
+  }
   TK_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o7, k_decompress<PlainChunks>, THREADS, 64 * sizeof(uint32_t)));
   if (occ < 1) return fail(c, TK_ERR_CUDA, "k_compress cannot be resident");
   c->occ_dec = (uint32_t)std::max(1, o7);
@@ -355,7 +368,7 @@ void free_all(tk_ctx* c) {
   void* ptrs[] = {c->cp.idx, c->cp.bits, c->cp.cnt, c->cta_sum, c->cta_max, c->cta_cls, c->cta_suffix, c->totals,
                   c->bar, c->wcnt,
                   c->ctrl, c->send, c->recv,
-                  c->recv_row, c->seg, c->h_g, c->h_r, c->h_out};
+                  c->recv_row, c->seg, c->h_g, c->h_r, c->h_out, c->dev_err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->prof_ev) {
@@ -404,13 +417,14 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if (k.n_iters < 1 || k.n_iters > (uint32_t)NMAX) return TK_ERR_INVALID_ARG;
   if (k.nranks < 1 || k.rank >= k.nranks) return TK_ERR_INVALID_ARG;
   if (k.rand_mode > 1 || k.step4 > 1 || k.levels_per_pass > 10 || k.rs_mode > 1 ||
-      k.ag_mode > 1 || k.select > 1 || k.wire > 1)
+      k.ag_mode > 1 || k.select > 2 || k.wire > 1 || k.exact_trial_counts > 1 || k.disable_ef_compaction > 1 ||
+      k.first_pass_keys > 3 || k.check_selection > 1 || k.loopback > 1)
     return TK_ERR_INVALID_ARG;
   const uint32_t n = k.group_size == 0 ? 1 : k.group_size;
   if (k.nranks % n != 0) return TK_ERR_CONFIG;
   if (k.d % n != 0) return TK_ERR_CONFIG;
   if (n > 1 && (k.d / n) % 4 != 0) return TK_ERR_CONFIG;  // segments start 16-byte aligned (128-bit access)
-  if (k.nranks > 1 && !uid) return TK_ERR_CONFIG;
+  if (k.nranks > 1 && !uid && !k.loopback) return TK_ERR_CONFIG;
   if (n > 1 && k.rs_mode == TK_RS_ORDERED && n != 2 && n != 4 && n != 8) return TK_ERR_CONFIG;
   if (n == 1 && k.ag_mode == TK_AG_PUSH && k.nranks > 8) return TK_ERR_CONFIG;
   const uint64_t L = k.d / n;
@@ -438,8 +452,7 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   // the whole vector.  Scratch is sized for the worst case (all passes on the whole vector).
   {
     // first pass: up to 3 keys along the predicted path (at least one level resolved)
-    uint32_t keys = 3;  // tuning knob (TK_FIRST_KEYS=1..3); results do not depend on it
-    if (const char* e = getenv("TK_FIRST_KEYS")) keys = std::max(1, std::min(3, atoi(e)));
+    const uint32_t keys = k.first_pass_keys == 0 ? 3u : k.first_pass_keys;  // results do not depend on it
     const uint32_t first = std::min<uint32_t>(std::min<uint32_t>(keys, c->levels), k.n_iters);
     c->lev_sched[0] = (int)first;
     const uint32_t per = std::min<uint32_t>(2u, c->levels);
@@ -447,10 +460,12 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
     // exact selector: <= 2 compacting passes + <= 16 whole-vector passes (2 bits each over the
     // 31-bit key space) + <= 4 histogram passes (8 bits each) + the final per-warp count
     if (k.select == TK_SELECT_EXACT) c->npass = 24;
-    else c->npass += k.n_iters;  // an ef-phase search (>= 1 level per pass) may precede a restart
-    if (const char* e = getenv("TK_EF_COMPACT")) c->ef_compact = atoi(e) != 0 ? 1u : 0u;
-    if (const char* e = getenv("TK_CHECK")) c->debug_check = atoi(e) != 0 ? 1u : 0u;
-    if (const char* e = getenv("TK_EF_COMPACT_PEERS")) c->ef_compact_peers = atoi(e) != 0 ? 1u : 0u;
+    // an ef-phase search (>= 1 level per pass) may precede a restart; exact_trial_counts adds up
+    // to ceil(NMAX / 8) whole-vector count passes
+    else c->npass += k.n_iters + (NMAX + 7) / 8;
+    c->ef_compact = k.disable_ef_compaction ? 0u : 1u;
+    c->debug_check = k.check_selection;
+    c->timeout_ns = (uint64_t)(k.push_timeout_ms == 0 ? 300000u : k.push_timeout_ms) * 1000000ull;
   }
   auto bail = [&](tk_status s) {
     free_all(c);
@@ -466,17 +481,22 @@ tk_status tk_init(const tk_config* cfg, const uint8_t* uid, tk_stream_t stream, 
   if ((s = plan_launches(c)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->wcnt, (size_t)c->npass * TMAX * c->W)) != TK_OK) return bail(s);
   if ((s = dev_alloc(c, &c->ctrl, 1)) != TK_OK) return bail(s);
+  if ((s = dev_alloc(c, &c->dev_err, 1)) != TK_OK) return bail(s);
+  if (cudaMemset(c->dev_err, 0, sizeof(uint32_t)) != cudaSuccess) return bail(TK_ERR_CUDA);
   c->cw = (k.wire == TK_WIRE_F16) ? kk + (kk + 1) / 2 : 2 * kk;
   if ((s = dev_alloc(c, &c->send, c->cw)) != TK_OK) return bail(s);
   const uint32_t chunks_recv = (n == 1) ? c->P : c->m;
   if ((s = dev_alloc(c, &c->recv, (size_t)chunks_recv * c->cw)) != TK_OK) return bail(s);
+  // scratch segment: the NCCL reduce-scatter's output, or where the peer-sum kernel stores acc
+  // without error feedback (tk_compress_segment allocates it on first use in flat mode)
+  if (n > 1 && (k.rs_mode == TK_RS_NCCL || !k.error_feedback))
+    if ((s = dev_alloc(c, &c->seg, L)) != TK_OK) return bail(s);
   if (n > 1) {
-    if (k.rs_mode == TK_RS_NCCL && (s = dev_alloc(c, &c->seg, L)) != TK_OK) return bail(s);
     if (k.step4 == TK_STEP4_SPARSE)
       if ((s = dev_alloc(c, &c->recv_row, (size_t)n * c->m * c->cw)) != TK_OK) return bail(s);
   }
   if (cudaMemset(c->ctrl, 0, sizeof(Ctrl)) != cudaSuccess) return bail(TK_ERR_CUDA);
-  if (c->P > 1) {
+  if (c->P > 1 && !k.loopback) {
     ncclUniqueId id;
     memcpy(&id, uid, sizeof(id));
     if (ncclCommInitRank(&c->world, (int)c->P, id, (int)c->rank) != ncclSuccess) return bail(TK_ERR_NCCL);
@@ -505,6 +525,60 @@ tk_status tk_compress(tk_ctx* c, const float* g, float* r, uint32_t* idx, float*
   if ((const void*)g == (const void*)r) return fail(c, TK_ERR_INVALID_ARG, "g aliases r");
   TK_TRY(compress_impl(c, g, ef ? r : nullptr, idx, val));
   return TK_OK;
+}
+
+tk_status tk_compress_segment(tk_ctx* c, const float* const* src, uint32_t nsrc, float* r, uint32_t* idx,
+                              float* val) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  const bool ef = c->cfg.error_feedback != 0;
+  if (!src || !idx || !val || (ef && !r)) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  if (nsrc != 1 && nsrc != 2 && nsrc != 4 && nsrc != 8) return fail(c, TK_ERR_INVALID_ARG, "nsrc must be 1, 2, 4 or 8");
+  if (ef && !aligned16(r)) return fail(c, TK_ERR_INVALID_ARG, "r must be 16-byte aligned");
+  Peers pr;
+  memset(&pr, 0, sizeof(pr));
+  for (uint32_t q = 0; q < nsrc; ++q) {
+    if (!src[q]) return fail(c, TK_ERR_INVALID_ARG, "null source pointer");
+    if (!aligned16(src[q])) return fail(c, TK_ERR_INVALID_ARG, "source %u must be 16-byte aligned", q);
+    if (ef && (const void*)src[q] == (const void*)r) return fail(c, TK_ERR_INVALID_ARG, "a source aliases r");
+    pr.p[q] = src[q];
+  }
+  if (nsrc == 1) return compress_impl(c, src[0], ef ? r : nullptr, idx, val);
+  if (!ef && !c->seg) TK_TRY(dev_alloc(c, &c->seg, c->L));  // where the peer sum is stored without EF
+  return compress_impl(c, nullptr, ef ? r : nullptr, idx, val, &pr, (int)nsrc);
+}
+
+tk_status tk_loopback_push(tk_ctx* c, const float* g, float* r, uint32_t* chunk, void* const* slots, uint32_t nslots,
+                           uint32_t tag) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (!c->cfg.loopback) return fail(c, TK_ERR_STATE, "tk_loopback_push needs a loopback context");
+  if (c->n != 1) return fail(c, TK_ERR_STATE, "the fused all-gather is the flat mode's");
+  const bool ef = c->cfg.error_feedback != 0;
+  if (!g || !chunk || !slots || (ef && !r)) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  if (nslots < 1 || nslots > 8 || tag == 0) return fail(c, TK_ERR_INVALID_ARG, "nslots in [1, 8], tag != 0");
+  if (!aligned16(g) || (ef && !aligned16(r))) return fail(c, TK_ERR_INVALID_ARG, "misaligned pointer");
+  PushOut po;
+  memset(&po, 0, sizeof(po));
+  po.np = nslots;
+  po.me = c->rank;
+  po.tag = tag;
+  for (uint32_t q = 0; q < nslots; ++q) {
+    if (!slots[q] || !aligned16(slots[q])) return fail(c, TK_ERR_INVALID_ARG, "slot %u null or misaligned", q);
+    po.slot[q] = static_cast<ulonglong2*>(slots[q]);
+  }
+  const ChunkOut co = chunk_out(c, chunk);
+  return compress_impl(c, g, ef ? r : nullptr, chunk, co.val, nullptr, 0, &po, co.val16);
+}
+
+tk_status tk_loopback_decompress(tk_ctx* c, const void* packets, uint32_t nchunks, uint32_t tag, float* out,
+                                 uint32_t* plain_out) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (!c->cfg.loopback) return fail(c, TK_ERR_STATE, "tk_loopback_decompress needs a loopback context");
+  if (!packets || !out) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
+  if (!aligned16(out) || !aligned16(packets)) return fail(c, TK_ERR_INVALID_ARG, "misaligned pointer");
+  if (nchunks < 1 || nchunks > 4096 || tag == 0) return fail(c, TK_ERR_INVALID_ARG, "nchunks in [1, 4096], tag != 0");
+  const uint64_t len = (c->n == 1) ? c->d : c->L;
+  TaggedChunks src{static_cast<const ulonglong2*>(packets), c->k, tag, c->dev_err, c->timeout_ns};
+  return decompress_impl(c, src, nchunks, c->k, len, out, plain_out);
 }
 
 tk_status tk_sparse_allgather(tk_ctx* c, const uint32_t* idx, const float* val, uint32_t* gathered) {
@@ -546,6 +620,7 @@ tk_status tk_decompress(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, f
 // decompression (out may then be nullptr, except for HiTopKComm dense step 4, which needs it).
 static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint32_t* gathered, float* w, float lr) {
   const bool ef = c->cfg.error_feedback != 0;
+  if (c->cfg.loopback && c->P > 1) return fail(c, TK_ERR_STATE, "a loopback context has no communicators");
   if (!g || (!out && !w) || (ef && !r)) return fail(c, TK_ERR_INVALID_ARG, "null pointer");
   if (w && !aligned16(w)) return fail(c, TK_ERR_INVALID_ARG, "misaligned w");
   if (w && ((const void*)w == (const void*)g || (const void*)w == (const void*)r || (const void*)w == (const void*)out))
@@ -579,7 +654,7 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
       TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, co.val, nullptr, 0, &po, co.val16));
       c->push_seq++;
       mark(c, TK_STAGE_ALLGATHER);
-      TaggedChunks src{c->pg + parity * stride, c->k, po.tag};
+      TaggedChunks src{c->pg + parity * stride, c->k, po.tag, c->dev_err, c->timeout_ns};
       TK_TRY(decompress_impl(c, src, c->P, c->k, c->d, out, gat, w, lr));
     } else {
       TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, co.val, nullptr, 0, nullptr, co.val16));
@@ -720,9 +795,16 @@ tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
   st->compacted = h.cap_ok;
   st->n_compacted = h.n_compacted;
   st->ef_compacted = h.ef_used;
-  st->nnz_lower_bound = h.nnz_lb;
+  st->nnz_not_counted = c->cfg.select == TK_SELECT_EXACT ? 0ull : h.nnz_lb;
+  for (uint32_t i = 0; i < st->n_trials && i < (uint32_t)NMAX; ++i)
+    if (st->nnz_not_counted >> i & 1ull) st->nnz[i] = TK_NNZ_NOT_COUNTED;  // only "nnz > k" is known
   st->n_phases = std::min<uint32_t>(12, h.n_phase);
   for (int i = 0; i < 12; ++i) st->phase_ns[i] = h.phase_ns[i];
+  uint32_t terr = 0;
+  TK_CUDA(c, cudaMemcpy(&terr, c->dev_err, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  c->timeout_sticky |= terr;
+  if (c->timeout_sticky)
+    return fail(c, TK_ERR_TIMEOUT, "a peer's packets did not arrive within push_timeout_ms (aggregate invalid)");
   if (c->nonfinite_sticky) return fail(c, TK_ERR_NONFINITE, "non-finite value in acc (precondition, Q24)");
   return TK_OK;
 }
@@ -810,6 +892,7 @@ const char* tk_status_string(tk_status s) {
     case TK_ERR_NCCL: return "NCCL error";
     case TK_ERR_STATE: return "invalid state";
     case TK_ERR_NOMEM: return "out of device memory";
+    case TK_ERR_TIMEOUT: return "fused all-gather timed out waiting for a peer";
   }
   return "unknown status";
 }

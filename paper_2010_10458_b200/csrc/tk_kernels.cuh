@@ -88,7 +88,13 @@ struct Ctrl {
   uint32_t ef_key;       // compaction key of the NEXT call's ef phase (0: none), set at the end of a call
   uint32_t ef_used;      // this call's selection ran on the ef-phase entries
   uint32_t prev_key2;    // MSTopK: the previous call's key2
-  uint64_t nnz_lb;       // trials whose logged nnz is a lower bound (> k): below the ef-phase key
+  uint64_t nnz_lb;       // trials whose count was not taken (their key lay below the ef-phase key, so
+                         // only "nnz > k" is known); cleared when exact_trial_counts counts them
+  // prose search (TK_SELECT_PROSE, reading Q33): the next trial threshold pt and the bracket
+  // [lo, hi] in THRESHOLD units (Alg. 1's bisection keeps lo, hi in ratio units); lo / hi are
+  // only meaningful once set
+  double pt;
+  uint32_t lo_set, hi_set;
 };
 
 
@@ -168,6 +174,12 @@ struct TaggedChunks {  // [nchunks][k] tagged packets, written by the peers duri
   const ulonglong2* g;
   uint64_t k;
   uint32_t tag;
+  uint32_t* err;        // sticky timeout flag (device word, reported by tk_get_stats)
+  uint64_t timeout_ns;  // how long to wait for one packet before giving up
+  // A packet that never arrives (a peer that died, or one that stalls longer than the timeout)
+  // sets *err and yields NO_INDEX - which every consumer treats as "beyond this tile", so the
+  // kernel finishes (memory-safe, result invalid) instead of trapping the CUDA context; once the
+  // flag is set no further packet is waited for.
   __device__ __forceinline__ void get(uint32_t p, uint32_t j, uint32_t& i, float& v) const {
     const ulonglong2* a = g + (size_t)p * k + j;
     ulonglong2 x = ld_ll(a);
@@ -175,11 +187,21 @@ struct TaggedChunks {  // [nchunks][k] tagged packets, written by the peers duri
       uint64_t t0;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
       do {
-        __nanosleep(32);
+        if (*reinterpret_cast<volatile uint32_t*>(err)) {
+          i = NO_INDEX;
+          v = 0.0f;
+          return;
+        }
+        __nanosleep(64);
         x = ld_ll(a);
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > 5000000000ull) __trap();  // a peer never delivered (5 s): fail loudly, never hang
+        if (t - t0 > timeout_ns) {
+          atomicExch(err, 1u);
+          i = NO_INDEX;
+          v = 0.0f;
+          return;
+        }
       } while ((uint32_t)(x.x >> 32) != tag || (uint32_t)(x.y >> 32) != tag);
     }
     i = (uint32_t)x.x;
@@ -220,17 +242,54 @@ __device__ __forceinline__ uint32_t key_of(double t) {
   return __float_as_uint(__double2float_ru(t));
 }
 
-// Candidates of one count pass: the 2^lev - 1 ratios of the next lev bisection levels below the
-// current [lo, hi], ascending.  Every ratio is dyadic with <= 52 significant bits, so
-// lo + (hi-lo)*m/2^lev is exact and equals the sequential l + (r-l)/2 of Alg. 1 l.8 (Q5).
+// Selectors of the compression kernel: Alg. 1 (MSTopK), the exact top-k of Eq. 2 and
+// MSTopK with the threshold search the prose of P:148 describes (reading Q33).
+enum { SEL_MSTOPK = 0, SEL_EXACT = 1, SEL_PROSE = 2 };
+
+// Prose search (Q33), one trial's outcome: nnz > k ("too many": the bracket's low end
+// moves up to t) or nnz <= k (its high end moves down to t); then the next trial is 2t while no
+// trial has had nnz <= k, t/2 while none has had nnz > k, else the fp64 midpoint of the bracket.
+// fmax / fmin are exact; 2t and t/2 are exact in fp64 here (|t| between 2^-200 and 2^200).
+__device__ __forceinline__ void prose_advance(double& t, double& lo, double& hi, uint32_t& lo_set, uint32_t& hi_set,
+                                              bool gt) {
+  if (gt) { lo = lo_set ? fmax(lo, t) : t; lo_set = 1u; }
+  else    { hi = hi_set ? fmin(hi, t) : t; hi_set = 1u; }
+  if (!hi_set) t = __dmul_rn(t, 2.0);
+  else if (!lo_set) t = __dmul_rn(t, 0.5);
+  else t = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), 0.5));
+}
+
+// Candidates of one count pass: the 2^lev - 1 trial keys of the next lev levels of the search
+// tree below the current state, in in-order (= ascending threshold) order.
+//   Alg. 1: the ratios lo + (hi-lo)*m/2^lev; every ratio is dyadic with <= 52 significant bits,
+//   so this is exact and equals the sequential l + (r-l)/2 of Alg. 1 l.8 (Q5).
+//   Prose: candidate m's threshold is found by walking from the root, taking at each node the
+//   decision that leads toward m (left = nnz <= k = smaller thresholds), with the same fp64
+//   operations the replay performs - so the keys are bit-identical to the trials' keys.
 // Computed by the CTA's threads in parallel (candidate m-1 by thread m-1); the caller
 // synchronises the CTA before and after.
+template <int SEL>
 __device__ void make_candidates_par(Ctrl* c, int lev) {
   const int T = (1 << lev) - 1;  // <= 1023
-  const double w = __dsub_rn(c->hi, c->lo);
-  for (int m = (int)threadIdx.x + 1; m <= T; m += THREADS) {
-    const double ratio = __dadd_rn(c->lo, __dmul_rn(w, (double)m * ldexp(1.0, -lev)));
-    c->cand_key[m - 1] = key_of(threshold_of(c->abar, c->U, ratio));
+  if constexpr (SEL == SEL_PROSE) {
+    for (int m = (int)threadIdx.x + 1; m <= T; m += THREADS) {
+      double t = c->pt, lo = c->lo, hi = c->hi;
+      uint32_t ls = c->lo_set, hs = c->hi_set;
+      int node = (T + 1) >> 1, half = node >> 1;
+      while (node != m) {
+        const bool gt = m > node;
+        prose_advance(t, lo, hi, ls, hs, gt);
+        node += gt ? half : -half;
+        half >>= 1;
+      }
+      c->cand_key[m - 1] = key_of(t);
+    }
+  } else {
+    const double w = __dsub_rn(c->hi, c->lo);
+    for (int m = (int)threadIdx.x + 1; m <= T; m += THREADS) {
+      const double ratio = __dadd_rn(c->lo, __dmul_rn(w, (double)m * ldexp(1.0, -lev)));
+      c->cand_key[m - 1] = key_of(threshold_of(c->abar, c->U, ratio));
+    }
   }
   if (threadIdx.x == 0) {
     c->ncand = (uint32_t)T;
@@ -239,25 +298,31 @@ __device__ void make_candidates_par(Ctrl* c, int lev) {
 }
 
 // Replay lev levels of Alg. 1 l.8-23 on the candidates' exact counts.
+template <int SEL>
 __device__ int replay_levels(Ctrl* c, const uint32_t* totals, int max_lev, int pass, uint64_t k) {
-  // Alg. 1 l.8-23, one level at a time: the level's ratio l + (r-l)/2 (exact, Q5) is looked up
-  // among the counted candidates; the replay stops at the first level whose threshold was not
-  // counted (speculative candidate sets).  Returns the number of levels resolved.
+  // Alg. 1 l.8-23, one level at a time: the level's trial (Alg. 1: ratio l + (r-l)/2, exact, Q5;
+  // prose: the state's next threshold) is looked up among the counted candidates; the replay
+  // stops at the first level whose threshold was not counted (speculative candidate sets).
+  // Returns the number of levels resolved.
   const int nc = (int)c->ncand;
   // a complete subtree (make_candidates_par: 2^L - 1 ascending candidates) is walked by index;
-  // other sets (the first pass's path) are searched
+  // other sets (the first pass's path) are searched by their coordinate (ratio / threshold)
   const bool tree = ((nc + 1) & nc) == 0 && c->cand_tree;
   int m = (nc + 1) >> 1, stepm = m >> 1;  // tree walk: 1-based node index and half-width
   int l = 0;
   for (; l < max_lev; ++l) {
-    const double ratio = __dadd_rn(c->lo, __dmul_rn(__dsub_rn(c->hi, c->lo), 0.5));  // Alg. 1 l.8
+    double ratio, t;
+    if constexpr (SEL == SEL_PROSE) {
+      ratio = c->pt;  // the prose search's coordinate is the threshold itself
+    } else {
+      ratio = __dadd_rn(c->lo, __dmul_rn(__dsub_rn(c->hi, c->lo), 0.5));  // Alg. 1 l.8
+    }
     int s = -1;
-    double t;
     if (tree) {
-      // node m of the complete subtree is exactly this level's midpoint (dyadic, Q5): its
-      // threshold and key are recomputed by the same operations make_candidates_par used
+      // node m of the complete subtree is exactly this level's trial: its threshold and key
+      // are recomputed by the same operations make_candidates_par used
       if (m >= 1 && m <= nc) s = m - 1;
-      t = threshold_of(c->abar, c->U, ratio);
+      t = (SEL == SEL_PROSE) ? ratio : threshold_of(c->abar, c->U, ratio);
     } else {
       for (int q = 0; q < nc && q < NPATH_CAND; ++q)
         if (c->cand_ratio[q] == ratio) { s = q; break; }
@@ -267,44 +332,66 @@ __device__ int replay_levels(Ctrl* c, const uint32_t* totals, int max_lev, int p
     const uint32_t nnz = totals[s];
     const uint32_t key = c->cand_key[s];
     const uint32_t it = c->it;
-    c->ratio_log[it] = ratio;
+    c->ratio_log[it] = (SEL == SEL_PROSE) ? __longlong_as_double(0x7FF8000000000000ll) : ratio;  // prose: no ratio
     c->thres_log[it] = t;
     c->key_log[it] = key;
     c->nnz_log[it] = nnz;
     c->it = it + 1;
-    if ((uint64_t)nnz <= k) {            // l.11
-      c->hi = ratio;                     // l.12
+    const bool gt = (uint64_t)nnz > k;
+    if (!gt) {                           // l.11
+      if constexpr (SEL != SEL_PROSE) c->hi = ratio;  // l.12
       if (nnz > c->k1) {                 // l.13
         c->k1 = nnz; c->thres1 = t; c->key1 = key; c->prov1 = pass * TMAX + s;
       }
       m -= stepm;
     } else {                             // l.17
-      c->lo = ratio;                     // l.18
+      if constexpr (SEL != SEL_PROSE) c->lo = ratio;  // l.18
       if (nnz < c->k2) {                 // l.19
         c->k2 = nnz; c->thres2 = t; c->key2 = key; c->prov2 = pass * TMAX + s;
       }
       m += stepm;
     }
+    if constexpr (SEL == SEL_PROSE) prose_advance(c->pt, c->lo, c->hi, c->lo_set, c->hi_set, gt);
     stepm >>= 1;
   }
   return l;
 }
 
-// Speculative candidates of the first pass: the lev bisection nodes along the path toward
-// `target` (the bracket the previous compression ended in).  When the data take that path, one
-// read of the vector resolves lev levels with lev keys; otherwise it resolves at least one.
+// Speculative candidates of the first pass: the lev search nodes along the path toward `target`
+// (the bracket the previous compression ended in, as a coordinate: ratio for Alg. 1, threshold
+// for the prose search).  When the data take that path, one read of the vector resolves lev
+// levels with lev keys; otherwise it resolves at least one.
+template <int SEL>
 __device__ void make_candidates_path(Ctrl* c, int lev, double target) {
-  double lo = c->lo, hi = c->hi;
-  for (int q = 0; q < lev; ++q) {
-    const double ratio = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), 0.5));
-    const double t = threshold_of(c->abar, c->U, ratio);
-    c->cand_ratio[q] = ratio;
-    c->cand_t[q] = t;
-    c->cand_key[q] = key_of(t);
-    if (target >= ratio) lo = ratio; else hi = ratio;
+  if constexpr (SEL == SEL_PROSE) {
+    double t = c->pt, lo = c->lo, hi = c->hi;
+    uint32_t ls = c->lo_set, hs = c->hi_set;
+    for (int q = 0; q < lev; ++q) {
+      c->cand_ratio[q] = t;
+      c->cand_t[q] = t;
+      c->cand_key[q] = key_of(t);
+      prose_advance(t, lo, hi, ls, hs, target >= t);
+    }
+  } else {
+    double lo = c->lo, hi = c->hi;
+    for (int q = 0; q < lev; ++q) {
+      const double ratio = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), 0.5));
+      const double t = threshold_of(c->abar, c->U, ratio);
+      c->cand_ratio[q] = ratio;
+      c->cand_t[q] = t;
+      c->cand_key[q] = key_of(t);
+      if (target >= ratio) lo = ratio; else hi = ratio;
+    }
   }
   c->ncand = (uint32_t)lev;
   c->cand_tree = 0u;
+}
+
+// the search bracket's low end (as a coordinate) lies at or above x: every later trial does too
+template <int SEL>
+__device__ __forceinline__ bool bracket_low_at_least(const Ctrl* c, double x) {
+  if constexpr (SEL == SEL_PROSE) return c->lo_set && c->lo >= x;
+  return c->lo >= x;
 }
 
 // Alg. 1 l.27 window: R = len(iota2) - (k - k1) + 1 >= 1 (Q8, Q9); rand uniform on [0, R).
@@ -398,8 +485,9 @@ __device__ __forceinline__ uint32_t quad_max_bits(float4 v) {
 // Candidates of the whole-vector first count pass: the nodes along the path toward the bracket
 // the previous compression ended in; the compaction key is the highest of them at or below that
 // bracket (any choice is exact; a good one keeps few elements).  One thread.
+template <int SEL>
 __device__ void first_pass_candidates(Ctrl* sc, int first_levels) {
-  make_candidates_path(sc, first_levels, sc->prev_lo);
+  make_candidates_path<SEL>(sc, first_levels, sc->prev_lo);
   int ms = 0;
   for (int q = 1; q < (int)sc->ncand; ++q)
     if (sc->cand_ratio[q] <= sc->prev_lo && sc->cand_ratio[q] > sc->cand_ratio[ms]) ms = q;
@@ -408,7 +496,7 @@ __device__ void first_pass_candidates(Ctrl* sc, int first_levels) {
       if (sc->cand_ratio[q] < sc->cand_ratio[ms]) ms = q;
   }
   // the compaction key becomes candidate 0, so the first pass's compaction test is the same
-  // compare as its count of that key (the replay finds candidates by ratio, order-free)
+  // compare as its count of that key (the replay finds candidates by coordinate, order-free)
   if (ms != 0) {
     const double r0 = sc->cand_ratio[0], t0 = sc->cand_t[0];
     const uint32_t k0 = sc->cand_key[0];
@@ -419,7 +507,8 @@ __device__ void first_pass_candidates(Ctrl* sc, int first_levels) {
   sc->cmp_ratio = sc->cand_ratio[0];
 }
 
-// Alg. 1 l.4-6: the search state before the first trial
+// Alg. 1 l.4-6: the search state before the first trial (prose: trial 1 at t = a-bar, no bracket)
+template <int SEL>
 __device__ __forceinline__ void search_reset(Ctrl* c, uint64_t n) {
   c->lo = 0.0; c->hi = 1.0;                             // l.4
   c->k1 = 0u; c->k2 = (uint32_t)n;                      // l.5
@@ -427,18 +516,23 @@ __device__ __forceinline__ void search_reset(Ctrl* c, uint64_t n) {
   c->key1 = INF_BITS; c->key2 = 0u;                     // Q8 / Q9 sentinels
   c->prov1 = -1; c->prov2 = -1;
   c->it = 0u;
+  if constexpr (SEL == SEL_PROSE) {
+    c->lo = 0.0; c->hi = 0.0;
+    c->lo_set = 0u; c->hi_set = 0u;
+    c->pt = c->abar;                                    // "we first use the average value"
+  }
 }
 
-__device__ void stats_finalize(Ctrl* c, const SearchParams& sp, double S, uint32_t m, uint64_t step,
-                               int first_levels) {
-  c->prev_lo = c->lo;
+template <int SEL>
+__device__ void stats_finalize(Ctrl* c, const SearchParams& sp, double S, uint32_t m, uint64_t step) {
+  // the previous call's final bracket low end predicts this call's (prose: 0 when never set)
+  c->prev_lo = (SEL == SEL_PROSE && !c->lo_set) ? 0.0 : c->lo;
   c->abar = __ddiv_rn(S, (double)sp.n);                 // Alg. 1 l.2
   c->umax_bits = m;                                     // Alg. 1 l.3
   c->U = (double)__uint_as_float(m);
   c->nonfinite = (m >= INF_BITS) ? 1u : 0u;
-  search_reset(c, sp.n);
+  search_reset<SEL>(c, sp.n);
   c->step = step;
-  (void)first_levels;
 }
 
 // HiTopKComm step 1 fused into K1 (Eq. 4; reading Q20): with NP > 0 the gradient of
@@ -494,13 +588,17 @@ __device__ __forceinline__ void ef_load(const float* g, const Peers& pr, const f
 // Optional compaction (ckey > 0, a key predicted by the previous call): every element with
 // bits(|acc|) >= ckey is appended, in index order, to the warp's entries at the BOTTOM of its
 // region ([0, cnt)); the warp's units are exactly its count-pass slab.  Per-CTA entry totals go
-// to cta_ent, a warp holding more than the capacity sets *overflow.
+// to cta_ent, a warp holding more than the capacity writes this launch's sequence number to
+// *overflow (a flag that is never cleared, so no CTA can wipe another's report).
+// acc is stored to accw when it is not already in memory: EF (accw = r, in place) and the
+// HiTopKComm peer sum (NP > 0; accw = r with EF, else a segment scratch buffer).
 template <bool EF, int NP>
-__device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peers& pr, float* __restrict__ r,
-                                         const SearchParams& sp, uint32_t units_per_warp,
+__device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peers& pr, const float* r,
+                                         float* accw, const SearchParams& sp, uint32_t units_per_warp,
                                          double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max,
-                                         uint32_t ckey, const Compact cp, uint32_t* overflow,
+                                         uint32_t ckey, const Compact cp, uint32_t* overflow, uint32_t seq,
                                          uint32_t* __restrict__ cta_ent) {
+  constexpr bool STORE = EF || NP > 0;
   __shared__ double s_ws[WARPS];
   __shared__ uint32_t s_wm[WARPS];
   __shared__ uint32_t s_we[WARPS];
@@ -556,11 +654,13 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
       }
       if (EF) {
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        for (int ch = 0; ch < 4; ++ch)
           acc[ch] = make_float4(__fadd_rn(acc[ch].x, rv[ch].x), __fadd_rn(acc[ch].y, rv[ch].y),
                                 __fadd_rn(acc[ch].z, rv[ch].z), __fadd_rn(acc[ch].w, rv[ch].w));
-          *reinterpret_cast<float4*>(r + base + ch * 128) = acc[ch];
-        }
+      }
+      if (STORE) {
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) *reinterpret_cast<float4*>(accw + base + ch * 128) = acc[ch];
       }
     } else {
 #pragma unroll
@@ -572,10 +672,8 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
           float x = 0.0f;  // zero leaves beyond n (padding of the canonical tree)
           if (idx < n) {
             x = load_g1<NP>(g, pr, idx);
-            if (EF) {
-              x = __fadd_rn(x, r[idx]);
-              r[idx] = x;
-            }
+            if (EF) x = __fadd_rn(x, r[idx]);
+            if (STORE) accw[idx] = x;
           }
           v[e] = x;
         }
@@ -663,7 +761,7 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
     s_we[warp] = ncomp;
     if (cmp_on) {
       cp.cnt[gw] = ncomp;
-      if (ncomp > cp.C) atomicOr(overflow, 1u);
+      if (ncomp > cp.C) atomicExch(overflow, seq);
     }
   }
   __syncthreads();
@@ -684,6 +782,7 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
 // Root of the canonical tree (every CTA computes it, identically, after the grid barrier):
 // the CTA partials zero-padded to Lp = 2^j >= THREADS leaves (extra zero leaves never change a
 // pairwise sum of non-negatives, Q3), then a-bar, u and the first pass's candidates.
+template <int SEL>
 __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* __restrict__ cta_max,
                            const SearchParams& sp, Ctrl* sc, uint64_t step, int first_levels) {
   __shared__ double s_v[THREADS];
@@ -729,10 +828,10 @@ __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* _
   if (tid == 0) {
     uint32_t m = s_m[0];
     for (int w = 1; w < WARPS; ++w) m = max(m, s_m[w]);
-    stats_finalize(sc, sp, s_v[0], m, step, first_levels);
+    stats_finalize<SEL>(sc, sp, s_v[0], m, step);
   }
   __syncthreads();
-  if (tid == 0) first_pass_candidates(sc, first_levels);
+  if (tid == 0) first_pass_candidates<SEL>(sc, first_levels);
   __syncthreads();
 }
 
@@ -752,7 +851,7 @@ enum { COUNT_FIRST = 0, COUNT_CAP = 1, COUNT_FULL = 2 };
 template <int NK, int MODE>
 __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const Ctrl* sc, const SearchParams sp,
                                             uint32_t* __restrict__ wcnt, const Compact cp, uint32_t* totals,
-                                            uint32_t* overflow, int pass) {
+                                            uint32_t* overflow, uint32_t seq, int pass) {
   constexpr int T = NK;  // keys counted in this pass
   __shared__ uint32_t s_cnt[WARPS][16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -896,7 +995,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
 #undef TK_LOAD
     if (MODE == COUNT_FIRST && lane == 0) {
       cp.cnt[gw] = ncomp;
-      if (ncomp > cp.C) atomicOr(overflow, 1u);
+      if (ncomp > cp.C) atomicExch(overflow, seq);
     }
   }
   // warp totals -> per-slab counts and the CTA's contribution to the pass totals
@@ -1241,7 +1340,9 @@ struct Fused {
   const float* g;            // gradient (flat) - unused when the peers supply it
   Peers pr;                  // HiTopKComm ordered reduce-scatter sources
   float* r;                  // residual in, acc / r' out (EF); nullptr without EF
-  const float* acc;          // the vector MSTopK reads: r (EF) or g
+  float* accw;               // where the ef phase stores acc: r (EF), a scratch segment (peer sum
+                             // without EF), nullptr (acc = g)
+  const float* acc;          // the vector MSTopK reads: accw or g
   uint32_t units_per_warp;   // ef phase: aligned power-of-two run of 512-element units per warp
   double* cta_sum;           // [grid] ef partials
   uint32_t* cta_max;         // [grid]
@@ -1249,7 +1350,11 @@ struct Fused {
   uint32_t* totals;          // [npass][16] global trial counts
   uint32_t* cta_cls;         // [2][grid] per-CTA class-1 / class-2 counts
   uint32_t* bar;             // grid barrier: [0] arrivals, [1] generation
-  uint32_t* flags;           // [0] compaction overflow
+  uint32_t* flags;           // overflow flags [0] first pass, [1] exact retry, [2] ef phase: each holds
+                             // the sequence number of the last launch that overflowed (never cleared)
+  uint32_t seq;              // this launch's sequence number (never 0)
+  uint32_t exact_counts;     // count every trial exactly (an extra whole-vector pass when the fast
+                             // search skipped the counts of trials below the ef-phase key)
   Compact cp;
   uint32_t* idx_out;
   float* val_out;
@@ -1293,7 +1398,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 template <int NK, int MODE>
 __device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass) {
-  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * HREP * pass, f.flags, pass);
+  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * HREP * pass, f.flags, f.seq, pass);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1302,7 +1407,6 @@ __device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass) {
 // space with the same count / compaction / histogram passes: T = the largest key with
 // #{a >= key} >= k.  Then class 1 = {a > T} (all kept), class 2 = {a == T} with the window at 0
 // (the lowest indices), i.e. key1 = T + 1, key2 = T, rand = 0 in the MSTopK selection.
-enum { SEL_MSTOPK = 0, SEL_EXACT = 1 };
 
 // bracket update from counted keys (one thread)
 __device__ __forceinline__ void exact_update(Ctrl* c, const uint32_t* keys, const uint32_t* cnt, int nk, uint64_t k) {
@@ -1328,6 +1432,7 @@ __device__ __forceinline__ uint32_t exact_split(const Ctrl* c, uint32_t j, uint3
 
 template <bool EF, int NP, int SEL>
 __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
+  static_assert(SEL == SEL_MSTOPK || SEL == SEL_EXACT || SEL == SEL_PROSE, "selector");
   __shared__ Ctrl sc;
   __shared__ uint32_t s_tot[HIST_BINS];
   __shared__ HistSmem s_hist;
@@ -1346,19 +1451,19 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   for (int i = blockIdx.x * THREADS + tid; i < HIST_BINS * HREP * f.max_pass; i += gridDim.x * THREADS)
     f.totals[i] = 0u;
   if (blockIdx.x == 0 && tid == 0) {
-    f.flags[0] = 0u; f.flags[1] = 0u; f.flags[2] = 0u;
     if (f.val16_out && (f.sp.k & 1u)) f.val16_out[f.sp.k] = 0u;  // FP16 wire: the chunk's padding half
   }
   // ---- A1-A2: error feedback, |acc| pairwise tree and max; compaction at the key the previous
   // call predicted (its entries replace the whole-vector first count pass when they are exact) ----
   const uint32_t efk = f.ef_compact ? sc.ef_key : 0u;
   uint32_t* cta_ent = f.cta_cls + 3 * gridDim.x;
-  ef_phase<EF, NP>(f.g, f.pr, f.r, f.sp, f.units_per_warp, f.cta_sum, f.cta_max, efk, f.cp, f.flags + 2, cta_ent);
+  ef_phase<EF, NP>(f.g, f.pr, f.r, f.accw, f.sp, f.units_per_warp, f.cta_sum, f.cta_max, efk, f.cp, f.flags + 2,
+                   f.seq, cta_ent);
   grid_sync(f.bar);
   stamp();
-  stats_root(f.cta_sum, f.cta_max, f.sp, &sc, f.step, f.lev0);
+  stats_root<SEL>(f.cta_sum, f.cta_max, f.sp, &sc, f.step, f.lev0);
   stamp();
-  const bool ef_ok = efk > 0u && __ldcg(f.flags + 2) == 0u;  // entries = {a >= efk}, none dropped
+  const bool ef_ok = efk > 0u && __ldcg(f.flags + 2) != f.seq;  // entries = {a >= efk}, none dropped
   bool nobar = false;  // the cross-CTA prefix comes from the published histogram suffixes (no barrier)
   if (tid == 0) { sc.cmp_bottom = 0u; sc.cap_ok = 0u; sc.ef_used = 0u; sc.nnz_lb = 0ull; }
   __syncthreads();
@@ -1425,7 +1530,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       load_totals(f.totals, 3, s_tot);
       if (tid == 0) {
         exact_update(&sc, sc.cand_key, s_tot, 3, k);
-        sc.cap_ok = ((uint64_t)s_tot[0] >= k && __ldcg(f.flags) == 0u) ? 1u : 0u;
+        sc.cap_ok = ((uint64_t)s_tot[0] >= k && __ldcg(f.flags) != f.seq) ? 1u : 0u;
         sc.it = 1u;
       }
       __syncthreads();
@@ -1463,7 +1568,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         }
         __syncthreads();
         if (mode == 1)
-          count_phase<3, COUNT_FIRST>(f.acc, &sc, f.sp, f.wcnt, f.cp, tot_p, f.flags + 1, p);
+          count_phase<3, COUNT_FIRST>(f.acc, &sc, f.sp, f.wcnt, f.cp, tot_p, f.flags + 1, f.seq, p);
         else
           run_count<3, COUNT_FULL>(f, &sc, p);
       }
@@ -1484,7 +1589,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
           sc.xguess = 0u;
         } else {
           exact_update(&sc, sc.cand_key, s_tot, 3, k);
-          if (mode == 1) sc.cap_ok = (__ldcg(f.flags + 1) == 0u) ? 1u : 0u;
+          if (mode == 1) sc.cap_ok = (__ldcg(f.flags + 1) != f.seq) ? 1u : 0u;
         }
         sc.it += 1u;
       }
@@ -1545,7 +1650,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     int done = 0;
     int p = p0;
     if (fast) {
-      make_candidates_par(&sc, min(min(HIST_LEV, f.cap_levels), N));
+      make_candidates_par<SEL>(&sc, min(min(HIST_LEV, f.cap_levels), N));
       __syncthreads();
     }
     for (; done < N; ++p) {
@@ -1586,11 +1691,11 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       if (fast) stamp();
       if (tid == 0) {
         const double cmp_ratio = sc.cmp_ratio;
-        s_got = replay_levels(&sc, s_tot, min(lev, N - done), p, f.sp.k);
+        s_got = replay_levels<SEL>(&sc, s_tot, min(lev, N - done), p, f.sp.k);
         if (first) {
           // compacted mode is exact iff every later threshold (and thres2) lies above the compaction
-          // key: the bracket's lower end must have reached its ratio, and nothing overflowed
-          sc.cap_ok = (sc.lo >= cmp_ratio && __ldcg(f.flags) == 0u) ? 1u : 0u;
+          // key: the bracket's lower end must have reached its coordinate, and nothing overflowed
+          sc.cap_ok = (bracket_low_at_least<SEL>(&sc, cmp_ratio) && __ldcg(f.flags) != f.seq) ? 1u : 0u;
         }
         if (done + s_got == N) finish_window(&sc, f.sp);
       }
@@ -1599,7 +1704,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       done += s_got;
       if (done < N) {
         const int next = sc.cap_ok ? min(min(HIST_LEV, f.cap_levels), N - done) : min(min(2, f.cap_levels), N - done);
-        make_candidates_par(&sc, next);
+        make_candidates_par<SEL>(&sc, next);
         __syncthreads();
       }
     }
@@ -1612,7 +1717,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     __syncthreads();
     pnext = search(0, true);
     if (tid == 0) {
-      s_got = (sc.prov2 >= 0 && sc.key2 >= efk) ? 1 : 0;
+      s_got = (sc.prov2 >= 0 && sc.key2 >= efk) ? 1 : 0;  // the search was exact (see above)
       uint64_t lb = 0;
       for (uint32_t i = 0; i < sc.it && i < (uint32_t)NMAX; ++i)
         if (sc.key_log[i] < efk) lb |= 1ull << i;
@@ -1624,14 +1729,44 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   nobar = ok && single;
   if (!ok) {
     if (tid == 0) {
-      search_reset(&sc, f.sp.n);
+      search_reset<SEL>(&sc, f.sp.n);
       sc.nnz_lb = 0ull;
       sc.cap_ok = 0u;
       sc.cmp_bottom = 0u;
-      first_pass_candidates(&sc, f.lev0);
+      first_pass_candidates<SEL>(&sc, f.lev0);
     }
     __syncthreads();
-    search(pnext, false);
+    pnext = search(pnext, false);
+  }
+  if (f.exact_counts) {
+    // exact_trial_counts: the trials the fast search only knows as "nnz > k" (key below the
+    // ef-phase key) are counted exactly, up to 8 per whole-vector pass, before the selection
+    // touches acc (Alg. 1 l.10 for every trial; the decisions were already exact)
+    __shared__ int s_tr[8];
+    __shared__ int s_nk;
+    while (sc.nnz_lb != 0ull) {
+      __syncthreads();
+      if (tid == 0) {
+        int nk = 0;
+        for (uint32_t i = 0; i < sc.it && i < (uint32_t)NMAX && nk < 8; ++i)
+          if (sc.nnz_lb >> i & 1ull) { s_tr[nk] = (int)i; sc.cand_key[nk] = sc.key_log[i]; ++nk; }
+        for (int q = nk; q < 8; ++q) sc.cand_key[q] = INF_BITS;  // counts nothing (finite input)
+        s_nk = nk;
+      }
+      __syncthreads();
+      run_count<8, COUNT_FULL>(f, &sc, pnext);
+      grid_sync(f.bar);
+      stamp();
+      load_totals(f.totals + HIST_BINS * HREP * pnext, 8, s_tot);
+      if (tid == 0) {
+        for (int q = 0; q < s_nk; ++q) {
+          sc.nnz_log[s_tr[q]] = s_tot[q];
+          sc.nnz_lb &= ~(1ull << s_tr[q]);
+        }
+      }
+      __syncthreads();
+      ++pnext;
+    }
   }
   if (tid == 0) {
     sc.ef_used = ok ? 1u : 0u;
@@ -1863,8 +1998,7 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
       if ((uint32_t)warp == (p & (WARPS - 1))) {
         uint32_t c0;
         if (p < WARPS) {
-          if (pi < thi) {
-            TK_DCHECK(pi >= tlo, "dec-pre", pi, tlo);
+          if (pi < thi && pi >= tlo) {  // (pi < tlo only for a packet that timed out: memory safety)
             s_tile[pi - tlo] = __fadd_rn(s_tile[pi - tlo], pv);
             emit(p, cur + lane, pi, pv);
           }
@@ -1879,8 +2013,7 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
             float v = 0.0f;
             if (j < k) src.get(p, j, i, v);
             const bool in = i < thi;
-            if (in) {
-              TK_DCHECK(i >= tlo, "dec-loop", i, tlo);
+            if (in && i >= tlo) {
               s_tile[i - tlo] = __fadd_rn(s_tile[i - tlo], v);
               emit(p, j, i, v);
             }

@@ -32,15 +32,24 @@ def _f32bits(t):
     return t.cpu().numpy().astype(np.float32).view(np.uint32)
 
 
-def _check_stats(st, ref):
+NNZ_NOT_COUNTED = 0xFFFFFFFF
+
+
+def _check_stats(st, ref, exact_counts=True):
+    """Every field of the control block, bit for bit.  exact_counts (the parity suite's mode):
+    every trial's nnz equals the oracle's count.  Default mode: a trial whose threshold lay below the
+    EF-pass key reports NNZ_NOT_COUNTED and claims only nnz > k - checked exactly as claimed."""
     s = ref.sel
     assert st.mean == s.mean, (st.mean, s.mean)
     assert st.max_bits == int(np.float32(s.u).view(np.uint32))
     assert len(st.trials) == len(s.trials)
+    if exact_counts:
+        assert st.nnz_not_counted == 0
     for it, (a, b) in enumerate(zip(st.trials, s.trials)):
-        assert a[0] == b[0] and a[1] == b[1] and a[2] == b[2], (it, a, b)
-        if st.nnz_lower_bound >> it & 1:  # below the EF-pass compaction key: a lower bound, > k
-            assert s.k < a[3] <= b[3], (it, a, b)
+        same_ratio = (a[0] == b[0]) or (np.isnan(a[0]) and np.isnan(b[0]))  # prose search: no ratio
+        assert same_ratio and a[1] == b[1] and a[2] == b[2], (it, a, b)
+        if st.nnz_not_counted >> it & 1:
+            assert a[3] == NNZ_NOT_COUNTED and b[3] > s.k, (it, a, b)
         else:
             assert a[3] == b[3], (it, a, b)
     assert (st.k1, st.k2) == (s.k1, s.k2)
@@ -51,19 +60,21 @@ def _check_stats(st, ref):
 
 
 def _compress_case(tk, d, dist, k, N, *, ef=True, seed=0, step=0, rank=0, rand_mode="seeded", levels=0, cfg=1,
-                   r_scale=0.0):
+                   r_scale=0.0, select="mstopk"):
     g = gradgen.gradient(d, dist, cfg=cfg, rank=rank, step=step)
     r = (gradgen.gradient(d, "G", cfg=cfg + 100, rank=rank, step=step) * np.float32(r_scale)).astype(np.float32)
-    ctx = tk.Context(d, k=k, n_iters=N, seed=seed, rand_mode=rand_mode, error_feedback=ef, levels_per_pass=levels)
+    ctx = tk.Context(d, k=k, n_iters=N, seed=seed, rand_mode=rand_mode, error_feedback=ef, levels_per_pass=levels,
+                     select=select, exact_trial_counts=True)
     ctx.set_step(step)
     gd, rd = _dev(g), _dev(r)
     idx, val = ctx.compress(gd, rd if ef else None)
     torch.cuda.synchronize()
     ref = oracle.compress(g, r if ef else None, k, N, seed=seed, step=step, rank=rank,
                           rand_mode=oracle.RAND_FIRST if rand_mode == "first" else oracle.RAND_SEEDED,
-                          error_feedback=ef)
+                          error_feedback=ef, selector=select)
     st = ctx.stats()
-    _check_stats(st, ref)
+    if select != "exact":
+        _check_stats(st, ref)
     assert np.array_equal(_u32(idx), ref.sel.idx)
     assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32))
     if ef:
@@ -120,7 +131,8 @@ def test_compress_no_error_feedback_and_first_mode(tk):
 def test_compress_worked_examples(tk, golden, case):
     gd = golden(case)
     x = np.array(gd["x"], np.float32)
-    ctx = tk.Context(len(x), k=gd["k"], n_iters=gd["N"], rand_mode="first", error_feedback=False)
+    ctx = tk.Context(len(x), k=gd["k"], n_iters=gd["N"], rand_mode="first", error_feedback=False,
+                     exact_trial_counts=True)
     idx, val = ctx.compress(_dev(x))
     st = ctx.stats()
     assert [(t[0], t[1], t[3]) for t in st.trials] == [tuple(t) for t in gd["trials"]]
@@ -129,7 +141,7 @@ def test_compress_worked_examples(tk, golden, case):
 
 def test_error_feedback_multi_step(tk):
     d, k, N = 200003, 200, 10
-    ctx = tk.Context(d, k=k, n_iters=N, seed=77)
+    ctx = tk.Context(d, k=k, n_iters=N, seed=77, exact_trial_counts=True)
     r_ref = np.zeros(d, np.float32)
     rd = _dev(r_ref)
     for step in range(4):
@@ -226,7 +238,7 @@ def test_compress_full_size_c2(tk, step):
     k = oracle.k_from_density(d, rho)
     r = (gradgen.gradient(d, "G", cfg=2, step=99) * np.float32(0.3 * step)).astype(np.float32)
     g = gradgen.gradient(d, "G", cfg=2, step=step)
-    ctx = tk.Context(d, rho=rho, n_iters=N, seed=1234)
+    ctx = tk.Context(d, rho=rho, n_iters=N, seed=1234, exact_trial_counts=True)
     ctx.set_step(step)
     rd = _dev(r)
     idx, val = ctx.compress(_dev(g), rd)
@@ -241,7 +253,7 @@ def test_compress_full_size_c3(tk):
     """BASELINE config 3's gradient (d = 110M, rho = 1e-3) on one rank, two EF steps."""
     d, rho, N = 110_000_000, 0.001, 10
     k = oracle.k_from_density(d, rho)
-    ctx = tk.Context(d, rho=rho, n_iters=N, seed=77)
+    ctx = tk.Context(d, rho=rho, n_iters=N, seed=77, exact_trial_counts=True)
     r = np.zeros(d, np.float32)
     rd = _dev(r)
     for step in range(2):
@@ -260,10 +272,12 @@ def test_compress_full_size_c3(tk):
 _EF_PATHS = set()
 
 
-def _multi_step(tk, d, dist, k, N, steps, *, scales=None, levels=0, seed=12, cfg=60):
+def _multi_step(tk, d, dist, k, N, steps, *, scales=None, levels=0, seed=12, cfg=60, exact_counts=True,
+                select="mstopk", expect_ef=False):
     """consecutive compressions on one context: from the second call on, the EF pass compacts at a
     key predicted by the previous call; every call is compared with the oracle bit for bit"""
-    ctx = tk.Context(d, k=k, n_iters=N, seed=seed, levels_per_pass=levels)
+    ctx = tk.Context(d, k=k, n_iters=N, seed=seed, levels_per_pass=levels, exact_trial_counts=exact_counts,
+                     select=select)
     r = np.zeros(d, np.float32)
     rd = _dev(r)
     for step in range(steps):
@@ -272,9 +286,11 @@ def _multi_step(tk, d, dist, k, N, steps, *, scales=None, levels=0, seed=12, cfg
             g = (g * np.float32(scales[step])).astype(np.float32)
         ctx.set_step(step)
         idx, val = ctx.compress(_dev(g), rd)
-        ref = oracle.compress(g, r, k, N, seed=seed, step=step)
+        ref = oracle.compress(g, r, k, N, seed=seed, step=step, selector=select)
         st = ctx.stats()
-        _check_stats(st, ref)
+        _check_stats(st, ref, exact_counts)
+        if expect_ef and step > 0:
+            assert st.ef_compacted, step  # the timed path: the EF pass compacted at the predicted key
         assert np.array_equal(_u32(idx), ref.sel.idx), step
         assert np.array_equal(_f32bits(val), ref.sel.val.view(np.uint32)), step
         assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32)), step
@@ -282,6 +298,7 @@ def _multi_step(tk, d, dist, k, N, steps, *, scales=None, levels=0, seed=12, cfg
             _EF_PATHS.add(st.ef_compacted)
         r = ref.residual
     ctx.close()
+    return st
 
 
 @pytest.mark.parametrize("dist", ["G", "L", "H", "ties8", "spike"])
@@ -305,3 +322,126 @@ def test_ef_compaction_paths_exercised(tk):
     _multi_step(tk, 100_003, "G", 100, 10, 3)
     _multi_step(tk, 100_003, "G", 100, 10, 4, scales=[1, 1, 1e4, 1])
     assert _EF_PATHS == {True, False}
+
+
+# ------------------------------------------------------------------ the bench's timed path at full size
+@pytest.mark.parametrize("dist", ["G", "L"])
+def test_full_size_c2_multi_step_ef_compacted(tk, dist):
+    """BASELINE config 2 at full size (d = 25.6M, rho = 1e-3, N = 10) on ONE context for 6 steps with
+    the residual carried - the regime bench.py times: from step 1 on the EF pass compacts at the
+    predicted key (asserted) and every trial is counted exactly (exact_trial_counts)."""
+    _multi_step(tk, 25_600_000, dist, 25_600, 10, 6, cfg=2, expect_ef=True)
+
+
+def test_full_size_c2_default_mode(tk):
+    """The same in the bench's default mode (no extra count pass): identical selection, residual and
+    control block; the trials whose count was skipped are flagged and exceed k in the oracle."""
+    st = _multi_step(tk, 25_600_000, "G", 25_600, 10, 4, cfg=3, exact_counts=False, expect_ef=True)
+    assert st.ef_compacted
+
+
+def test_default_and_exact_count_modes_agree_on_skipped_trials(tk):
+    # a case where trials do fall below the EF-pass key: both modes bit-identical, the default one flags them
+    d, k = 2_000_003, 2000
+    flagged = 0
+    for exact in (False, True):
+        ctx = tk.Context(d, k=k, n_iters=10, seed=3, exact_trial_counts=exact)
+        r = torch.zeros(d, device="cuda")
+        for step in range(4):
+            ctx.set_step(step)
+            ctx.compress(_dev(gradgen.gradient(d, "G", cfg=4, step=step)), r)
+            st = ctx.stats()
+            if not exact:
+                flagged |= st.nnz_not_counted
+            else:
+                assert st.nnz_not_counted == 0 and NNZ_NOT_COUNTED not in [t[3] for t in st.trials]
+        ctx.close()
+    assert flagged != 0  # the fast search did skip counts in the default mode
+
+
+# ------------------------------------------------------------------ prose search (SURVEY F3, P:148, Q33)
+@pytest.mark.parametrize("d", [1, 5, 129, 4097, 65537, (1 << 20) + 3])
+def test_prose_edge_sizes(tk, d):
+    _compress_case(tk, d, "G", max(1, d // 100), 10, r_scale=0.1, select="prose")
+
+
+@pytest.mark.parametrize("dist", gradgen.DISTS)
+@pytest.mark.parametrize("d,rho,N", [(1000, 0.01, 10), (300001, 0.001, 20), (100000, 0.01, 5)])
+def test_prose_distributions(tk, dist, d, rho, N):
+    _compress_case(tk, d, dist, oracle.k_from_density(d, rho), N, seed=3, step=1, r_scale=0.05, select="prose")
+
+
+@pytest.mark.parametrize("levels", [1, 2, 4, 10])
+@pytest.mark.parametrize("N", [1, 3, 10, 30, 52])
+def test_prose_levels_per_pass_invariance(tk, levels, N):
+    _compress_case(tk, 50003, "L", 50, N, levels=levels, seed=5, select="prose")
+
+
+@pytest.mark.parametrize("k", [1, 2, 9999, 10000])
+def test_prose_k_extremes(tk, k):
+    _compress_case(tk, 10000, "H", k, 10, seed=9, select="prose")
+
+
+def test_prose_no_ef_and_first_mode(tk):
+    _compress_case(tk, 1_000_000, "G", 1000, 10, ef=False, select="prose")
+    _compress_case(tk, 77777, "ties8", 77, 10, rand_mode="first", select="prose")
+    _compress_case(tk, 4096, "zero", 40, 10, select="prose")
+
+
+def test_prose_hand_worked_examples(tk):
+    # the trial sequences of tests/test_oracle_prose.py, worked by hand from P:148
+    x = np.array([1, -2, 3, 4, -5, 6, 7, -8], np.float32)
+    ctx = tk.Context(8, k=2, n_iters=4, rand_mode="first", error_feedback=False, select="prose",
+                     exact_trial_counts=True)
+    idx, val = ctx.compress(_dev(x))
+    st = ctx.stats()
+    assert [t[1] for t in st.trials] == [4.5, 9.0, 6.75, 5.625] and [t[3] for t in st.trials] == [4, 0, 2, 3]
+    assert _u32(idx).tolist() == [6, 7] and val.cpu().tolist() == [7.0, -8.0]
+    x = np.array([100, 1, -1, 1], np.float32)
+    ctx = tk.Context(4, k=3, n_iters=6, rand_mode="first", error_feedback=False, select="prose",
+                     exact_trial_counts=True)
+    idx, _ = ctx.compress(_dev(x))
+    assert [t[1] for t in ctx.stats().trials] == [25.75, 12.875, 6.4375, 3.21875, 1.609375, 0.8046875]
+    assert _u32(idx).tolist() == [0, 1, 2]
+
+
+@pytest.mark.parametrize("dist", ["G", "L", "H"])
+def test_prose_multi_step_ef_compaction(tk, dist):
+    _multi_step(tk, 300_001, dist, 300, 10, 5, select="prose", cfg=61)
+
+
+def test_prose_restart_on_shift(tk):
+    _multi_step(tk, 400_003, "G", 400, 10, 6, scales=[1, 1, 1000, 1e-3, 1e-3, 1], select="prose", cfg=62)
+
+
+def test_prose_full_size_c2(tk):
+    """F3's bench configuration: C2 at full size, 4 steps on one context, EF-pass compaction."""
+    _multi_step(tk, 25_600_000, "G", 25_600, 10, 4, select="prose", cfg=63, expect_ef=True)
+
+
+# ------------------------------------------------------------------ all-zero input (reading Q34)
+@pytest.mark.parametrize("rand_mode", ["first", "seeded"])
+def test_all_zero_input_worked_example(tk, golden, rand_mode):
+    gd = golden("E9_all_zero.json")
+    x = np.array(gd["x"], np.float32)
+    ctx = tk.Context(len(x), k=gd["k"], n_iters=gd["N"], rand_mode=rand_mode, error_feedback=False,
+                     exact_trial_counts=True)
+    idx, val = ctx.compress(_dev(x))
+    st = ctx.stats()
+    assert [(t[0], t[1], t[3]) for t in st.trials] == [tuple(t) for t in gd["trials"]]
+    assert (st.k1, st.k2, st.len2, st.thres1_set, st.thres2_set) == (gd["k1"], gd["k2"], gd["len2"], False, False)
+    ref = oracle.mstopk(x, gd["k"], gd["N"], rand_mode=oracle.RAND_FIRST if rand_mode == "first" else 0)
+    assert st.rand == ref.rand and _u32(idx).tolist() == ref.idx.tolist()
+    assert _f32bits(val).tolist() == ref.val.view(np.uint32).tolist()
+    if rand_mode == "first":
+        assert _u32(idx).tolist() == gd["first_idx"] and _f32bits(val).tolist() == gd["first_val_bits"]
+
+
+@pytest.mark.parametrize("select", ["mstopk", "prose", "exact"])
+def test_all_zero_input_large(tk, select):
+    if select == "exact":
+        ctx = tk.Context(100_000, k=100, n_iters=10, select="exact")
+        idx, _ = ctx.compress(torch.zeros(100_000, device="cuda"), torch.zeros(100_000, device="cuda"))
+        assert _u32(idx).tolist() == list(range(100))  # Eq. 2 with every |x| tied: the lowest indices
+        return
+    _compress_case(tk, 100_000, "zero", 100, 10, select=select)

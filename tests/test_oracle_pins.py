@@ -123,6 +123,93 @@ def test_splitmix64_published_stream():
     assert got == want
 
 
+def test_window_hash_chain_vector():
+    """H(s,t,p,c) = sm(sm(sm(sm(s)^t)^p)^c) (reading Q10) on inputs chosen so that every stage's
+    input is a state of the published seed-0 SplitMix64 stream: sm(x) = mix(x + gamma) and the
+    stream's outputs are O_i = mix(i * gamma), so sm(0) = O1, sm(gamma) = O2, sm(2 gamma) = O3.
+    Then H(0, O1^gamma, O2^(2 gamma), O3^gamma) = sm(gamma) = O2 - a chained vector pinned only by
+    published numbers; a dropped, repeated or reordered XOR stage breaks it."""
+    M = (1 << 64) - 1
+    gamma = 0x9E3779B97F4A7C15
+    O1, O2, O3 = 0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F
+    t, p, c = O1 ^ gamma, O2 ^ ((2 * gamma) & M), O3 ^ gamma
+    assert oracle.window_hash(0, t, p, c) == O2
+    # each stage alone: the chain passes through exactly the published states
+    assert oracle.window_hash(0, t, p, c) != oracle.window_hash(0, p, t, c)  # step and rank are not symmetric
+    assert oracle.window_hash(0, t, (2 * gamma) & M, 0) != O2
+    # rand = floor(H * R / 2^64) (Lemire multiply-high, Q10): H = O2 over R = 6 windows
+    assert (O2 * 6) >> 64 == 2
+
+
+def test_e9_all_zero_worked_example(golden):
+    g = golden("E9_all_zero.json")
+    x = np.array(g["x"], np.float32)
+    assert (x.view(np.uint32) >> 31).tolist() == g["x_sign_bits"]
+    res = oracle.mstopk(x, g["k"], g["N"], rand_mode=RAND_FIRST)
+    assert res.mean == g["mean"] and res.u == g["u"]
+    assert [(t[0], t[1], t[3]) for t in res.trials] == [tuple(t) for t in g["trials"]]
+    assert (res.k1, res.k2, res.thres1_set, res.thres2_set, res.len2) == (g["k1"], g["k2"], False, False, g["len2"])
+    assert res.len2 - (g["k"] - res.k1) + 1 == g["R"]
+    assert res.idx.tolist() == g["first_idx"] and res.val.view(np.uint32).tolist() == g["first_val_bits"]
+    # seeded mode: a contiguous run of k indices starting at the drawn window position
+    res = oracle.mstopk(x, g["k"], g["N"], seed=7, step=3)
+    assert res.idx.tolist() == list(range(res.rand, res.rand + g["k"])) and 0 <= res.rand < g["R"]
+
+
+def _alg1_literal(xs, k, N, seed, step, rank):
+    """Algorithm 1 transcribed line by line in plain Python (lists, Python floats,
+    no numpy), with the readings Q3 (recursive pairwise mean), Q8 (k1 = 0 guard), Q10 (window RNG),
+    Q11 (ascending output) - an independent second transcription for small d."""
+    d = len(xs)
+    a = [abs(v) for v in xs]                                   # l.1
+    D = 1
+    while D < d:
+        D *= 2
+
+    def pw(lo, hi):
+        if hi - lo == 1:
+            return a[lo] if lo < d else 0.0
+        mid = (lo + hi) // 2
+        return pw(lo, mid) + pw(mid, hi)
+    abar = pw(0, D) / d                                        # l.2
+    u = max(a)                                                 # l.3
+    l, r = 0.0, 1.0                                            # l.4
+    k1, k2 = 0, d                                              # l.5
+    thres1, thres2 = 0.0, 0.0                                  # l.6
+    trials = []
+    for _ in range(N):                                         # l.7
+        ratio = l + (r - l) / 2                                # l.8
+        thres = abar + ratio * (u - abar)                      # l.9
+        nnz = sum(1 for v in a if v >= thres)                  # l.10
+        trials.append((ratio, thres, nnz))
+        if nnz <= k:                                           # l.11
+            r = ratio                                          # l.12
+            if nnz > k1:                                       # l.13
+                k1, thres1 = nnz, thres                        # l.14-15
+        elif nnz > k:                                          # l.17
+            l = ratio                                          # l.18
+            if nnz < k2:                                       # l.19
+                k2, thres2 = nnz, thres                        # l.20-21
+    iota1 = [i for i in range(d) if k1 > 0 and a[i] >= thres1]                       # l.25 (Q8)
+    iota2 = [i for i in range(d) if not (k1 > 0 and a[i] >= thres1) and a[i] >= thres2]  # l.26
+    R = len(iota2) - (k - k1) + 1
+    rand = (oracle.window_hash(seed, step, rank, 0) * R) >> 64  # l.27 (Q10)
+    iota = sorted(iota1 + iota2[rand:rand + k - k1])           # l.28 (Q11)
+    return trials, k1, k2, thres1, thres2, iota, [xs[i] for i in iota]  # l.29
+
+
+@pytest.mark.parametrize("dist", ["G", "L", "H", "ties8", "const", "spike"])
+@pytest.mark.parametrize("d,k,N", [(1, 1, 3), (7, 2, 5), (100, 3, 10), (1000, 10, 10), (4096, 41, 20), (3001, 300, 52)])
+def test_alg1_trajectory_matches_literal_python(dist, d, k, N):
+    x = gradgen.gradient(d, dist, cfg=610, step=d)
+    xs = [float(v) for v in x]
+    trials, k1, k2, t1, t2, iota, vals = _alg1_literal(xs, k, N, seed=11, step=2, rank=1)
+    res = oracle.mstopk(x, k, N, seed=11, step=2, rank=1)
+    assert [(t[0], t[1], t[3]) for t in res.trials] == trials
+    assert (res.k1, res.k2, res.thres1, res.thres2) == (k1, k2, t1, t2)
+    assert res.idx.tolist() == iota and res.val.tolist() == vals
+
+
 # ---------------------------------------------------------------- mean: error bound / closed form
 @pytest.mark.parametrize("d", [1, 2, 3, 1000, 4097, 65536 + 5])
 def test_pairwise_sum_error_bound(d):
