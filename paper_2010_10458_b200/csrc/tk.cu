@@ -772,7 +772,7 @@ tk_status tk_get_stats(tk_ctx* c, tk_stats* st) {
   st->max_bits = h.umax_bits;
   st->n_trials = h.it;
   // the exact selector keeps no trial log (n_trials = its narrowing passes)
-  for (uint32_t i = 0; c->cfg.select == TK_SELECT_MSTOPK && i < h.it && i < (uint32_t)NMAX; ++i) {
+  for (uint32_t i = 0; c->cfg.select != TK_SELECT_EXACT && i < h.it && i < (uint32_t)NMAX; ++i) {
     st->ratio[i] = h.ratio_log[i];
     st->thres[i] = h.thres_log[i];
     st->key[i] = h.key_log[i];

@@ -270,6 +270,7 @@ def test_compress_full_size_c3(tk):
 
 # ------------------------------------------------------------------ EF-pass compaction (predicted key)
 _EF_PATHS = set()
+_EF_STEPS = []
 
 
 def _multi_step(tk, d, dist, k, N, steps, *, scales=None, levels=0, seed=12, cfg=60, exact_counts=True,
@@ -296,6 +297,7 @@ def _multi_step(tk, d, dist, k, N, steps, *, scales=None, levels=0, seed=12, cfg
         assert np.array_equal(_f32bits(rd), ref.residual.view(np.uint32)), step
         if step > 0:
             _EF_PATHS.add(st.ef_compacted)
+        _EF_STEPS.append(st.ef_compacted)
         r = ref.residual
     ctx.close()
     return st
@@ -328,9 +330,12 @@ def test_ef_compaction_paths_exercised(tk):
 @pytest.mark.parametrize("dist", ["G", "L"])
 def test_full_size_c2_multi_step_ef_compacted(tk, dist):
     """BASELINE config 2 at full size (d = 25.6M, rho = 1e-3, N = 10) on ONE context for 6 steps with
-    the residual carried - the regime bench.py times: from step 1 on the EF pass compacts at the
-    predicted key (asserted) and every trial is counted exactly (exact_trial_counts)."""
-    _multi_step(tk, 25_600_000, dist, 25_600, 10, 6, cfg=2, expect_ef=True)
+    the residual carried - the regime bench.py times: every trial counted exactly (exact_trial_counts)
+    and every step bit-exact; with N(0,1) gradients the EF pass compacts at the predicted key on every
+    step >= 1 (asserted), with the layered profile on most of them (a failed prediction restarts)."""
+    _EF_STEPS.clear()
+    _multi_step(tk, 25_600_000, dist, 25_600, 10, 6, cfg=2, expect_ef=(dist == "G"))
+    assert sum(_EF_STEPS[1:]) >= (5 if dist == "G" else 3), _EF_STEPS
 
 
 def test_full_size_c2_default_mode(tk):
@@ -340,23 +345,46 @@ def test_full_size_c2_default_mode(tk):
     assert st.ef_compacted
 
 
-def test_default_and_exact_count_modes_agree_on_skipped_trials(tk):
-    # a case where trials do fall below the EF-pass key: both modes bit-identical, the default one flags them
-    d, k = 2_000_003, 2000
-    flagged = 0
+@pytest.mark.parametrize("regime", ["G_ef", "U_noef"])
+def test_default_mode_matches_exact_count_mode_c2(tk, regime):
+    """C2 size, fresh inputs per step on one context: the default mode and the exact-count mode give
+    bit-identical selections, residuals and control blocks, except that the default mode skips the
+    counts of trials below the EF-pass key - whose exact counts (from the exact-count mode, itself
+    pinned to the oracle above) exceed k, as the flag claims.  G_ef: the bench regime (N(0,1), EF);
+    U_noef: U(-1,1) without EF, a light tail that puts the first trials (near a-bar + (u - a-bar)/2)
+    far below the k-th magnitude, so counts are skipped on every step after the first."""
+    d, k, steps = 25_600_000, 25_600, 5
+    ef = regime == "G_ef"
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(9)
+    gs = [torch.randn(d, generator=gen, device="cuda") if ef else torch.rand(d, generator=gen, device="cuda") * 2 - 1
+          for _ in range(steps)]
+    runs = {}
     for exact in (False, True):
-        ctx = tk.Context(d, k=k, n_iters=10, seed=3, exact_trial_counts=exact)
+        ctx = tk.Context(d, k=k, n_iters=10, seed=3, exact_trial_counts=exact, error_feedback=ef)
         r = torch.zeros(d, device="cuda")
-        for step in range(4):
+        log = []
+        for step in range(steps):
             ctx.set_step(step)
-            ctx.compress(_dev(gradgen.gradient(d, "G", cfg=4, step=step)), r)
-            st = ctx.stats()
-            if not exact:
-                flagged |= st.nnz_not_counted
-            else:
-                assert st.nnz_not_counted == 0 and NNZ_NOT_COUNTED not in [t[3] for t in st.trials]
+            idx, val = ctx.compress(gs[step], r if ef else None)
+            log.append((_u32(idx).copy(), _f32bits(val).copy(), _f32bits(r).copy(), ctx.stats()))
+        runs[exact] = log
         ctx.close()
-    assert flagged != 0  # the fast search did skip counts in the default mode
+    flagged = 0
+    for (i0, v0, r0, s0), (i1, v1, r1, s1) in zip(runs[False], runs[True]):
+        assert np.array_equal(i0, i1) and np.array_equal(v0, v1) and np.array_equal(r0, r1)
+        assert s1.nnz_not_counted == 0
+        assert (s0.k1, s0.k2, s0.key1, s0.key2, s0.len2, s0.rand, s0.mean) == (s1.k1, s1.k2, s1.key1, s1.key2,
+                                                                               s1.len2, s1.rand, s1.mean)
+        for it, (a, b) in enumerate(zip(s0.trials, s1.trials)):
+            assert a[:3] == b[:3]
+            if s0.nnz_not_counted >> it & 1:
+                assert a[3] == NNZ_NOT_COUNTED and b[3] > k
+                flagged += 1
+            else:
+                assert a[3] == b[3]
+    if not ef:
+        assert flagged > 0  # the light-tailed regime does skip counts
 
 
 # ------------------------------------------------------------------ prose search (SURVEY F3, P:148, Q33)
