@@ -50,8 +50,8 @@ struct tk_ctx {
   uint32_t* cta_cls = nullptr;        // [4][grid] per-CTA class counts, entries
   uint32_t* cta_suffix = nullptr;     // [grid][HIST_BINS] per-CTA histogram suffix sums
   uint32_t* totals = nullptr;         // [npass][HREP][256] pass totals / histograms
-  uint32_t* bar = nullptr;            // grid barrier words [2] + flags [2]
-  uint32_t* flags = nullptr;
+  uint64_t* bar = nullptr;            // grid barrier: monotonic arrival counter (never reset)
+  uint32_t* flags = nullptr;          // overflow flags [4] (launch sequence numbers)
   double* cta_sum = nullptr;          // K1 per-CTA partial sums / maxima
   uint32_t* cta_max = nullptr;
   uint32_t* wcnt = nullptr;           // per-warp-slab counts [npass*TMAX][W]
@@ -300,9 +300,10 @@ tk_status plan_launches(tk_ctx* c) {
   TK_TRY(dev_alloc(c, &c->cta_cls, 4 * (size_t)c->grid));
   TK_TRY(dev_alloc(c, &c->cta_suffix, (size_t)c->grid * HIST_BINS));
   TK_TRY(dev_alloc(c, &c->totals, (size_t)HIST_BINS * HREP * c->npass));
-  TK_TRY(dev_alloc(c, &c->bar, 8));
-  TK_CUDA(c, cudaMemset(c->bar, 0, 8 * sizeof(uint32_t)));
-  c->flags = c->bar + 2;
+  TK_TRY(dev_alloc(c, &c->bar, 1));
+  TK_CUDA(c, cudaMemset(c->bar, 0, sizeof(uint64_t)));
+  TK_TRY(dev_alloc(c, &c->flags, 4));
+  TK_CUDA(c, cudaMemset(c->flags, 0, 4 * sizeof(uint32_t)));
   // compacted entries: capacity S/4 per warp slab (the whole-vector path covers an overflow)
   c->cp.C = (uint32_t)std::max<uint64_t>(4, (c->S / 4 + 3) / 4 * 4);
   TK_TRY(dev_alloc(c, &c->cp.idx, (size_t)c->W * c->cp.C));
@@ -366,7 +367,7 @@ tk_status open_push_peers(tk_ctx* c) {
 
 void free_all(tk_ctx* c) {
   void* ptrs[] = {c->cp.idx, c->cp.bits, c->cp.cnt, c->cta_sum, c->cta_max, c->cta_cls, c->cta_suffix, c->totals,
-                  c->bar, c->wcnt,
+                  c->bar, c->flags, c->wcnt,
                   c->ctrl, c->send, c->recv,
                   c->recv_row, c->seg, c->h_g, c->h_r, c->h_out, c->dev_err};
   for (void* p : ptrs)

@@ -9,6 +9,7 @@
 //
 // Citations: P:n = PAPER.md line n.  Q<n> = numbered reading in DESIGN.md.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -44,8 +45,12 @@ constexpr int HIST_BINS = 1 << HIST_LEV;
 constexpr int TOT_STRIDE = HIST_BINS;  // words per copy
 constexpr int NPATH_CAND = 16;           // candidates with an explicit ratio / threshold (path, exact)
 
-// Device-resident MSTopK control block (Alg. 1 l.4-6 state + the trial log).
+// Device-resident MSTopK control block (Alg. 1 l.4-6 state + the trial log).  Laid out as
+//   [header: scalar state, incl. what the next call predicts from]  copied in by every CTA
+//   [logs: trial log, phase stamps]                                  written back by CTA 0
+//   [scratch: candidate keys of one pass]                            per call, never copied
 struct Ctrl {
+  // ---------------------------------------------------------------- header
   double abar;        // Alg. 1 l.2
   double U;           // (double) u, Alg. 1 l.3
   uint32_t umax_bits;
@@ -57,26 +62,16 @@ struct Ctrl {
   int32_t prov1, prov2;  // slot (pass*TMAX + candidate) whose per-warp counts are key1's / key2's; -1 unset
   uint32_t it;           // trials done
   uint32_t ncand;        // candidates of the pass about to run
-  uint32_t cand_key[HIST_BINS];  // candidate keys (ascending for a tree / histogram pass)
-  double cand_ratio[NPATH_CAND];    // ratio / threshold of path candidates (tree candidates are
-  double cand_t[NPATH_CAND];        // recomputed from lo, hi in the replay)
-  uint32_t ticket;
   uint32_t cap_ok;       // 1: passes >= 1 and the selection run on the compacted entries (see k_count)
   uint32_t cmp_key;      // key above which the first count pass compacts elements
   double cmp_ratio;      // its bisection ratio
   double prev_lo;        // final l of the previous compression (predicts the bracket; perf only)
-  uint32_t overflow;     // set by a warp whose compacted entries exceeded the capacity
   uint32_t need;
+  uint32_t n_phase;
   uint64_t len2;
   uint64_t rand;
   uint64_t step;
-  double ratio_log[NMAX];
-  double thres_log[NMAX];
-  uint32_t key_log[NMAX];
-  uint32_t nnz_log[NMAX];
-  uint64_t phase_ns[12];  // %globaltimer at the phase boundaries of the last k_compress (CTA 0)
-  uint32_t n_phase;
-  uint32_t n_compacted;  // entries kept by the first count pass (all warps)
+  uint32_t n_compacted;  // entries kept by the compaction (all warps)
   uint32_t cand_tree;    // the candidates form a complete subtree (walked by index in replay)
   // exact selector (TK_SELECT_EXACT): bracket [xlo, xhi) of the k-th largest key T with
   // xcnt_lo = #{a >= xlo} >= k > xcnt_hi = #{a >= xhi}; prev_T = the previous call's T (0: none)
@@ -95,7 +90,20 @@ struct Ctrl {
   // only meaningful once set
   double pt;
   uint32_t lo_set, hi_set;
+  // ---------------------------------------------------------------- logs
+  double ratio_log[NMAX];
+  double thres_log[NMAX];
+  uint32_t key_log[NMAX];
+  uint32_t nnz_log[NMAX];
+  uint64_t phase_ns[12];  // %globaltimer at the phase boundaries of the last k_compress (CTA 0)
+  // ---------------------------------------------------------------- per-call scratch
+  double cand_ratio[NPATH_CAND];    // coordinate (ratio / threshold) of path candidates
+  double cand_t[NPATH_CAND];        // and their thresholds
+  uint32_t cand_key[HIST_BINS];     // candidate keys (ascending for a tree / histogram pass)
 };
+constexpr int CTRL_HEADER_WORDS = (int)(offsetof(Ctrl, ratio_log) / 4);
+constexpr int CTRL_KEEP_WORDS = (int)(offsetof(Ctrl, cand_ratio) / 4);
+static_assert(offsetof(Ctrl, ratio_log) % 8 == 0 && offsetof(Ctrl, cand_ratio) % 8 == 0, "Ctrl layout");
 
 
 // Per-launch parameters of the MSTopK kernels.  The count and selection kernels share one
@@ -414,28 +422,17 @@ __device__ void finish_window(Ctrl* c, const SearchParams& sp) {
   c->rand = r;
 }
 
-// last-CTA-done ticket: true in every thread of the CTA that finished last (resets the ticket)
-__device__ __forceinline__ bool last_cta(uint32_t* ticket) {
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (s_last) __threadfence();
-  return s_last;
-}
-
 // The last CTA runs the scalar control on a shared-memory copy of the control block (one
 // coalesced load and store by the whole CTA instead of a chain of dependent global accesses).
 __device__ __forceinline__ void ctrl_to_smem(Ctrl* s, const Ctrl* g) {
   static_assert(sizeof(Ctrl) % 4 == 0, "Ctrl must be a whole number of words");
-  for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += blockDim.x)
+  for (int i = threadIdx.x; i < CTRL_HEADER_WORDS; i += blockDim.x)
     reinterpret_cast<uint32_t*>(s)[i] = __ldcg(reinterpret_cast<const uint32_t*>(g) + i);
   __syncthreads();
 }
 __device__ __forceinline__ void ctrl_to_global(Ctrl* g, const Ctrl* s) {
   __syncthreads();
-  for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += blockDim.x)
+  for (int i = threadIdx.x; i < CTRL_KEEP_WORDS; i += blockDim.x)
     reinterpret_cast<uint32_t*>(g)[i] = reinterpret_cast<const uint32_t*>(s)[i];
 }
 
@@ -472,16 +469,6 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 //   (tree over its 8 warps), and the last CTA folds the CTA partials (zero-padded to a power of
 //   two, Q3) into a-bar, u and the first pass's candidate thresholds.
 // HBM: 12 B/elem with EF (read g, read r, write acc), 4 B/elem without.
-__device__ __forceinline__ double lane_quad_sum(float4 v) {
-  return __dadd_rn(__dadd_rn((double)fabsf(v.x), (double)fabsf(v.y)),
-                   __dadd_rn((double)fabsf(v.z), (double)fabsf(v.w)));
-}
-__device__ __forceinline__ uint32_t quad_max_bits(float4 v) {
-  const uint32_t a = __float_as_uint(v.x) & 0x7FFFFFFFu, b = __float_as_uint(v.y) & 0x7FFFFFFFu;
-  const uint32_t c = __float_as_uint(v.z) & 0x7FFFFFFFu, d = __float_as_uint(v.w) & 0x7FFFFFFFu;
-  return max(max(a, b), max(c, d));
-}
-
 // Candidates of the whole-vector first count pass: the nodes along the path toward the bracket
 // the previous compression ended in; the compaction key is the highest of them at or below that
 // bracket (any choice is exact; a good one keeps few elements).  One thread.
@@ -544,6 +531,8 @@ struct Peers {
   const float* p[8];  // row peers' gradient + segment offset, in row-rank order
 };
 
+// The ef phase's unit is one warp round of 512 elements as four coalesced 128-element chunks:
+// lane l holds elements 4l..4l+3 of each chunk (one 128-bit load per chunk per source).
 template <int NP>
 __device__ __forceinline__ void load_g(const float* g, const Peers& pr, uint64_t base, float4* gv) {
   if (NP == 0) {
@@ -575,51 +564,96 @@ __device__ __forceinline__ float load_g1(const float* g, const Peers& pr, uint64
   return a;
 }
 
-template <bool EF, int NP>
-__device__ __forceinline__ void ef_load(const float* g, const Peers& pr, const float* r, uint64_t base, float4* gv,
-                                        float4* rv) {
-  load_g<NP>(g, pr, base, gv);
-  if (EF) {
-#pragma unroll
-    for (int ch = 0; ch < 4; ++ch) rv[ch] = __ldcs(reinterpret_cast<const float4*>(r + base + ch * 128));
+// Entries the ef phase keeps: staged per warp in shared memory; a warp whose entries outgrow the
+// staging buffer spills them, in order, to its global region (flushed > 0) - otherwise they stay in
+// shared memory for the count, prefix and selection phases of the same CTA (no global round trip).
+constexpr uint32_t SCAP = 256;
+struct EfStage {
+  uint32_t si[WARPS][SCAP];  // element index
+  uint32_t sb[WARPS][SCAP];  // bits of acc
+  uint32_t n[WARPS];         // entries of the warp
+  uint32_t in_smem[WARPS];   // 1: all of them are in si/sb (none spilled)
+};
+
+// A warp's compacted entries, wherever they are (ascending index order)
+struct Entries {
+  const uint32_t* idx;
+  const uint32_t* bits;
+  uint32_t n;
+  bool smem;
+  __device__ __forceinline__ uint32_t b(uint32_t j) const { return smem ? bits[j] : __ldcg(bits + j); }
+  __device__ __forceinline__ uint32_t i(uint32_t j) const { return smem ? idx[j] : __ldcg(idx + j); }
+  __device__ __forceinline__ uint4 b4(uint32_t j) const {
+    return smem ? make_uint4(bits[j], bits[j + 1], bits[j + 2], bits[j + 3]) : ldcg4(bits + j);
   }
+  __device__ __forceinline__ uint4 i4(uint32_t j) const {
+    return smem ? make_uint4(idx[j], idx[j + 1], idx[j + 2], idx[j + 3]) : ldcg4(idx + j);
+  }
+};
+__device__ __forceinline__ Entries warp_entries(const Compact& cp, const EfStage& es, uint32_t cmp_bottom, uint32_t gw,
+                                                int warp) {
+  Entries e;
+  if (cmp_bottom && es.in_smem[warp]) {
+    e.idx = es.si[warp];
+    e.bits = es.sb[warp];
+    e.n = es.n[warp];
+    e.smem = true;
+  } else {
+    e.n = min(__ldcg(cp.cnt + gw), cp.C);
+    const uint32_t off = entry_off(cp, e.n, cmp_bottom);
+    e.idx = cp.idx + (size_t)gw * cp.C + off;
+    e.bits = cp.bits + (size_t)gw * cp.C + off;
+    e.smem = false;
+  }
+  return e;
 }
 
+__device__ __forceinline__ double lane_quad_sum(float4 v) {
+  return __dadd_rn(__dadd_rn((double)fabsf(v.x), (double)fabsf(v.y)), __dadd_rn((double)fabsf(v.z), (double)fabsf(v.w)));
+}
+__device__ __forceinline__ uint32_t quad_max_bits(float4 v) {
+  const uint32_t a = __float_as_uint(v.x) & 0x7FFFFFFFu, b = __float_as_uint(v.y) & 0x7FFFFFFFu;
+  const uint32_t c = __float_as_uint(v.z) & 0x7FFFFFFFu, d = __float_as_uint(v.w) & 0x7FFFFFFFu;
+  return max(max(a, b), max(c, d));
+}
+
+// A1 + A2 (+ H1 when NP > 0): acc = (sum of the NP sources, or g) (+ r with EF), stored to accw
+// when not already in memory (EF: accw = r, in place; the HiTopKComm peer sum without EF: a
+// segment scratch), the canonical fp64 pairwise tree of |acc| (Q3) - lane: 4 leaves, xor-shuffle:
+// 128-leaf chunks, unit: 512, warp: aligned power-of-two run of units (binary-counter stack) - and
+// max |acc|.
 // Optional compaction (ckey > 0, a key predicted by the previous call): every element with
-// bits(|acc|) >= ckey is appended, in index order, to the warp's entries at the BOTTOM of its
-// region ([0, cnt)); the warp's units are exactly its count-pass slab.  Per-CTA entry totals go
-// to cta_ent, a warp holding more than the capacity writes this launch's sequence number to
-// *overflow (a flag that is never cleared, so no CTA can wipe another's report).
-// acc is stored to accw when it is not already in memory: EF (accw = r, in place) and the
-// HiTopKComm peer sum (NP > 0; accw = r with EF, else a segment scratch buffer).
+// bits(|acc|) >= ckey is appended, in index order, to the warp's entries (EfStage; spilled to the
+// BOTTOM of the warp's global region [0, cnt) if they outgrow it); the warp's units are exactly its
+// count-pass slab.  Per-CTA entry totals go to cta_ent; a warp holding more than the global
+// capacity writes this launch's sequence number to *overflow (a flag that is never cleared, so no
+// CTA can wipe another's report).
 template <bool EF, int NP>
 __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peers& pr, const float* r,
                                          float* accw, const SearchParams& sp, uint32_t units_per_warp,
                                          double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max,
                                          uint32_t ckey, const Compact cp, uint32_t* overflow, uint32_t seq,
-                                         uint32_t* __restrict__ cta_ent) {
+                                         uint32_t* __restrict__ cta_ent, EfStage& es) {
   constexpr bool STORE = EF || NP > 0;
   __shared__ double s_ws[WARPS];
   __shared__ uint32_t s_wm[WARPS];
-  __shared__ uint32_t s_we[WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t n = sp.n;
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint64_t u0 = (uint64_t)gw * units_per_warp;
   const bool cmp_on = ckey > 0u;
   const int32_t ckm1 = (int32_t)ckey - 1;
-  // hits are staged per warp in shared memory and written to the entries in coalesced runs
-  constexpr uint32_t SCAP = 256;
-  __shared__ uint32_t s_si[WARPS][SCAP], s_sb[WARPS][SCAP];
-  uint32_t staged = 0, flushed = 0;  // warp-uniform
+  uint32_t staged = 0, flushed = 0;  // warp-uniform: entries in the staging buffer / spilled
   uint32_t* oi = cp.idx + (size_t)gw * cp.C;
   uint32_t* ob = cp.bits + (size_t)gw * cp.C;
-  auto flush = [&]() {
+  uint32_t* si = es.si[warp];
+  uint32_t* sb = es.sb[warp];
+  auto spill = [&]() {
     __syncwarp();
     for (uint32_t j = lane; j < staged; j += 32)
       if (flushed + j < cp.C) {
-        oi[flushed + j] = s_si[warp][j];
-        ob[flushed + j] = s_sb[warp][j];
+        oi[flushed + j] = si[j];
+        ob[flushed + j] = sb[j];
       }
     flushed += staged;
     staged = 0;
@@ -627,32 +661,16 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   };
   double stk[24];
   uint32_t mx = 0;
-  // NP == 0: the next unit's loads are issued before this unit is reduced (one unit in flight
-  // ahead per warp); the peer-sum variant (NP > 0) keeps NP*4 loads per unit and no prefetch
-#ifndef TK_EF_PREF
-#define TK_EF_PREF 0
-#endif
-  constexpr bool PREF = TK_EF_PREF != 0;  // measured: prefetching does not help this phase
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 ng[4] = {z4, z4, z4, z4}, nr[4] = {z4, z4, z4, z4};
-  bool nfull = units_per_warp > 0 && (u0 + 1) * ROUND <= n;
-  if (PREF && nfull) ef_load<EF, NP>(g, pr, r, u0 * ROUND + 4 * lane, ng, nr);
   for (uint32_t i = 0; i < units_per_warp; ++i) {
     const uint64_t u = u0 + i;
     const uint64_t base = u * ROUND + 4 * lane;
     float4 acc[4];
-    const bool full = PREF ? nfull : ((u + 1) * ROUND <= n);
-    if (full) {
-      float4 rv[4];
-      if (PREF) {
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) { acc[ch] = ng[ch]; rv[ch] = nr[ch]; }
-        nfull = (i + 1 < units_per_warp) && (u + 2) * ROUND <= n;
-        if (nfull) ef_load<EF, NP>(g, pr, r, base + ROUND, ng, nr);
-      } else {
-        ef_load<EF, NP>(g, pr, r, base, acc, rv);
-      }
+    if ((u + 1) * ROUND <= n) {
+      load_g<NP>(g, pr, base, acc);
       if (EF) {
+        float4 rv[4];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) rv[ch] = __ldcs(reinterpret_cast<const float4*>(r + base + ch * 128));
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch)
           acc[ch] = make_float4(__fadd_rn(acc[ch].x, rv[ch].x), __fadd_rn(acc[ch].y, rv[ch].y),
@@ -679,10 +697,6 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
         }
         acc[ch] = make_float4(v[0], v[1], v[2], v[3]);
       }
-      if (PREF) {
-        nfull = (i + 1 < units_per_warp) && (u + 2) * ROUND <= n;
-        if (nfull) ef_load<EF, NP>(g, pr, r, base + ROUND, ng, nr);
-      }
     }
     if (cmp_on) {
       // element (ch, lane, e) has index u*512 + ch*128 + 4*lane + e: chunk-major, then lane, then
@@ -707,15 +721,14 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t excl = incl - packed;
         const uint32_t tu = (tot & 0xFFu) + ((tot >> 8) & 0xFFu) + ((tot >> 16) & 0xFFu) + (tot >> 24);
-        if (staged + tu > SCAP) flush();
-        // the unit's hits go to the warp's shared-memory staging buffer (or, if more than it
-        // holds, straight to the entries)
+        if (staged + tu > SCAP) spill();
+        // the unit's hits go to the warp's staging buffer (or, if more than it holds, straight to
+        // the global entries); only this lane's hits are visited (usually none or one): chunk
+        // ch's run starts at b0 + hits of the earlier chunks, then the earlier lanes' hits of
+        // chunk ch, then this lane's earlier hits in the chunk
         const bool direct = tu > SCAP;
         const uint32_t b0 = direct ? flushed : staged;
         const uint32_t t0 = tot & 0xFFu, t1 = (tot >> 8) & 0xFFu, t2 = (tot >> 16) & 0xFFu;
-        // only this lane's hits are visited (usually none or one): chunk ch's run starts at
-        // b0 + hits of the earlier chunks, then the earlier lanes' hits of chunk ch, then this
-        // lane's earlier hits in the chunk
         for (uint32_t mm = m; mm; mm &= mm - 1u) {
           const int j = __ffs(mm) - 1;
           const int ch = j >> 2, e = j & 3;
@@ -723,13 +736,12 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
           const uint32_t pos = cbase + ((excl >> (8 * ch)) & 0xFFu) + __popc(m & ((1u << j) - 1u) & (0xFu << (4 * ch)));
           const float4 a4 = ch == 0 ? acc[0] : (ch == 1 ? acc[1] : (ch == 2 ? acc[2] : acc[3]));
           const float av = e == 0 ? a4.x : (e == 1 ? a4.y : (e == 2 ? a4.z : a4.w));
-          const uint32_t i = (uint32_t)(u * ROUND + ch * 128 + 4 * lane + e);
+          const uint32_t ii = (uint32_t)(u * ROUND + ch * 128 + 4 * lane + e);
           if (direct) {
-            if (pos < cp.C) { oi[pos] = i; ob[pos] = __float_as_uint(av); }
+            if (pos < cp.C) { oi[pos] = ii; ob[pos] = __float_as_uint(av); }
           } else {
-            TK_DCHECK(pos < SCAP, "ef-stage", pos, staged);
-            s_si[warp][pos] = i;
-            s_sb[warp][pos] = __float_as_uint(av);
+            si[pos] = ii;
+            sb[pos] = __float_as_uint(av);
           }
         }
         if (direct) flushed += tu; else staged += tu;
@@ -750,15 +762,18 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
     for (uint32_t cnt = i; cnt & 1u; cnt >>= 1) v = __dadd_rn(stk[lvl++], v);  // binary-counter stack
     stk[lvl] = v;
   }
-  if (cmp_on) flush();
-  const uint32_t ncomp = flushed;
+  // entries that never left shared memory stay there; otherwise the rest follows the spilled ones
+  const bool in_smem = cmp_on && flushed == 0;
+  if (cmp_on && !in_smem) spill();
+  const uint32_t ncomp = flushed + staged;
   int top = 0;
   while ((1u << top) < units_per_warp) ++top;
   mx = __reduce_max_sync(0xffffffffu, mx);
   if (lane == 0) {
     s_ws[warp] = stk[top];
     s_wm[warp] = mx;
-    s_we[warp] = ncomp;
+    es.n[warp] = cmp_on ? ncomp : 0u;
+    es.in_smem[warp] = in_smem ? 1u : 0u;
     if (cmp_on) {
       cp.cnt[gw] = ncomp;
       if (ncomp > cp.C) atomicExch(overflow, seq);
@@ -768,7 +783,7 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   if (threadIdx.x == 0) {
     uint32_t te = 0;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) te += s_we[w];
+    for (int w = 0; w < WARPS; ++w) te += es.n[w];
     cta_ent[blockIdx.x] = te;
     cta_sum[blockIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(s_ws[0], s_ws[1]), __dadd_rn(s_ws[2], s_ws[3])),
                                     __dadd_rn(__dadd_rn(s_ws[4], s_ws[5]), __dadd_rn(s_ws[6], s_ws[7])));
@@ -784,15 +799,15 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
 // pairwise sum of non-negatives, Q3), then a-bar, u and the first pass's candidates.
 template <int SEL>
 __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* __restrict__ cta_max,
-                           const SearchParams& sp, Ctrl* sc, uint64_t step, int first_levels) {
+                           const uint32_t* __restrict__ cta_ent, const SearchParams& sp, Ctrl* sc, uint64_t step) {
   __shared__ double s_v[THREADS];
-  __shared__ uint32_t s_m[WARPS];
+  __shared__ uint32_t s_m[WARPS], s_n[WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t Lp = THREADS;
   while (Lp < gridDim.x) Lp <<= 1;
   const uint32_t G = Lp / THREADS;  // <= 8 for grids up to 2048 CTAs
   double leaf[8];
-  uint32_t m2 = 0;
+  uint32_t m2 = 0, ne = 0;
 #pragma unroll
   for (uint32_t q = 0; q < 8; ++q) {
     const uint32_t li = tid * G + q;
@@ -800,6 +815,7 @@ __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* _
     if (q < G && li < gridDim.x) {
       leaf[q] = __ldcg(cta_sum + li);
       m2 = max(m2, __ldcg(cta_max + li));
+      ne += __ldcg(cta_ent + li);
     }
   }
   double st2[4];
@@ -816,7 +832,8 @@ __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* _
   while ((1u << top2) < G) ++top2;
   s_v[tid] = st2[top2];
   m2 = __reduce_max_sync(0xffffffffu, m2);
-  if (lane == 0) s_m[warp] = m2;
+  ne = __reduce_add_sync(0xffffffffu, ne);
+  if (lane == 0) { s_m[warp] = m2; s_n[warp] = ne; }
   __syncthreads();
   for (int h = THREADS / 2; h >= 1; h >>= 1) {
     double v = 0.0;
@@ -826,12 +843,11 @@ __device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* _
     __syncthreads();
   }
   if (tid == 0) {
-    uint32_t m = s_m[0];
-    for (int w = 1; w < WARPS; ++w) m = max(m, s_m[w]);
+    uint32_t m = s_m[0], t = s_n[0];
+    for (int w = 1; w < WARPS; ++w) { m = max(m, s_m[w]); t += s_n[w]; }
     stats_finalize<SEL>(sc, sp, s_v[0], m, step);
+    sc->n_compacted = t;  // entries the ef phase kept (statistics)
   }
-  __syncthreads();
-  if (tid == 0) first_pass_candidates<SEL>(sc, first_levels);
   __syncthreads();
 }
 
@@ -851,7 +867,7 @@ enum { COUNT_FIRST = 0, COUNT_CAP = 1, COUNT_FULL = 2 };
 template <int NK, int MODE>
 __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const Ctrl* sc, const SearchParams sp,
                                             uint32_t* __restrict__ wcnt, const Compact cp, uint32_t* totals,
-                                            uint32_t* overflow, uint32_t seq, int pass) {
+                                            uint32_t* overflow, uint32_t seq, int pass, const EfStage& es) {
   constexpr int T = NK;  // keys counted in this pass
   __shared__ uint32_t s_cnt[WARPS][16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -872,8 +888,8 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
     for (int s = 0; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
   };
   if (MODE == COUNT_CAP) {
-    const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-    const uint32_t* eb = cp.bits + (size_t)gw * cp.C + entry_off(cp, ne, sc->cmp_bottom);
+    const Entries e = warp_entries(cp, es, sc->cmp_bottom, gw, warp);
+    const uint32_t ne = e.n;
     // this warp's entry loads in flight together (4 x 128 entries per iteration)
     for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
       uint4 q[4];
@@ -881,7 +897,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
       for (int u = 0; u < 4; ++u) {
         const uint32_t j = j0 + u * 128 + 4 * lane;
         q[u] = make_uint4(0u, 0u, 0u, 0u);
-        if (j + 4 <= ne) q[u] = ldcg4(eb + j);
+        if (j + 4 <= ne) q[u] = e.b4(j);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -889,7 +905,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
         if (j + 4 <= ne) {
           count1(q[u].x); count1(q[u].y); count1(q[u].z); count1(q[u].w);
         } else {
-          for (uint32_t t = j; t < ne && t < j + 4; ++t) count1(__ldcg(eb + t));
+          for (uint32_t t = j; t < ne && t < j + 4; ++t) count1(e.b(t));
         }
       }
     }
@@ -1030,7 +1046,7 @@ struct HistSmem {
 // grid barrier (#entries of CTA c at or above candidate s = S_c[s + 1]).
 template <int LEV>
 __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uint32_t* ghist, HistSmem& hs,
-                                           uint32_t* suf = nullptr) {
+                                           const EfStage& es, uint32_t* suf = nullptr) {
   constexpr int NB = 1 << LEV;
   const int32_t* s_key = reinterpret_cast<const int32_t*>(sc->cand_key);  // sorted, in shared memory
   uint32_t* s_h = hs.h;
@@ -1038,8 +1054,8 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
   for (int i = threadIdx.x; i < NB; i += THREADS) s_h[i] = 0u;
   __syncthreads();
   const uint32_t gw = blockIdx.x * WARPS + warp;
-  const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-  const uint32_t* eb = cp.bits + (size_t)gw * cp.C + entry_off(cp, ne, sc->cmp_bottom);
+  const Entries e = warp_entries(cp, es, sc->cmp_bottom, gw, warp);
+  const uint32_t ne = e.n;
   auto add = [&](uint32_t bits) {
     const int32_t a = (int32_t)(bits & 0x7FFFFFFFu);
     uint32_t b = 0;
@@ -1053,7 +1069,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
     for (int u = 0; u < 4; ++u) {
       const uint32_t j = j0 + u * 128 + 4 * lane;
       q[u] = make_uint4(0u, 0u, 0u, 0u);
-      if (j + 4 <= ne) q[u] = ldcg4(eb + j);
+      if (j + 4 <= ne) q[u] = e.b4(j);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -1061,7 +1077,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
       if (j + 4 <= ne) {
         add(q[u].x); add(q[u].y); add(q[u].z); add(q[u].w);
       } else {
-        for (uint32_t t = j; t < ne && t < j + 4; ++t) add(__ldcg(eb + t));
+        for (uint32_t t = j; t < ne && t < j + 4; ++t) add(e.b(t));
       }
     }
   }
@@ -1161,7 +1177,7 @@ __device__ __forceinline__ void put_sel(const SelOut& o, uint32_t pos, uint32_t 
 
 __device__ __forceinline__ void select_phase(const float* __restrict__ acc, const Ctrl* c, const SearchParams sp,
                                           uint32_t c1, uint32_t c2, uint32_t b1, uint32_t b2, const SelOut& so,
-                                          const Compact cp) {
+                                          const Compact cp, const EfStage& es) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint64_t lo = min(sp.n, (uint64_t)gw * sp.S);
@@ -1175,22 +1191,20 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
   if (c->cap_ok) {
     // ---- compacted entries of this warp (ascending index order): 128 per iteration, lane l
     // holds entries 4l..4l+3 of the group, so (lane, e) order is index order ----
-    const uint32_t ne = min(__ldcg(cp.cnt + gw), cp.C);
-    const uint32_t off = entry_off(cp, ne, c->cmp_bottom);
-    const uint32_t* ei = cp.idx + (size_t)gw * cp.C + off;
-    const uint32_t* eb = cp.bits + (size_t)gw * cp.C + off;
+    const Entries en = warp_entries(cp, es, c->cmp_bottom, gw, warp);
+    const uint32_t ne = en.n;
     for (uint32_t j0 = 0; j0 < ne; j0 += 128) {
       const uint32_t j = j0 + 4 * lane;
       uint32_t bb[4] = {0u, 0u, 0u, 0u}, ii[4] = {0u, 0u, 0u, 0u};
       if (j + 4 <= ne) {
-        const uint4 q = ldcg4(eb + j);
-        const uint4 x = ldcg4(ei + j);
+        const uint4 q = en.b4(j);
+        const uint4 x = en.i4(j);
         bb[0] = q.x; bb[1] = q.y; bb[2] = q.z; bb[3] = q.w;
         ii[0] = x.x; ii[1] = x.y; ii[2] = x.z; ii[3] = x.w;
       } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (j + e < ne) { bb[e] = __ldcg(eb + j + e); ii[e] = __ldcg(ei + j + e); }
+          if (j + e < ne) { bb[e] = en.b(j + e); ii[e] = en.i(j + e); }
       }
       uint32_t fc1 = 0, fc2 = 0;
 #pragma unroll
@@ -1349,7 +1363,7 @@ struct Fused {
   uint32_t* wcnt;            // [npass * TMAX][W] per-warp-slab trial counts
   uint32_t* totals;          // [npass][16] global trial counts
   uint32_t* cta_cls;         // [2][grid] per-CTA class-1 / class-2 counts
-  uint32_t* bar;             // grid barrier: [0] arrivals, [1] generation
+  uint64_t* bar;             // grid barrier: monotonic arrival counter
   uint32_t* flags;           // overflow flags [0] first pass, [1] exact retry, [2] ef phase: each holds
                              // the sequence number of the last launch that overflowed (never cleared)
   uint32_t seq;              // this launch's sequence number (never 0)
@@ -1370,24 +1384,43 @@ struct Fused {
   uint32_t wire16;           // FP16 wire values (F3): round the values sent, keep the error in r
 };
 
-// Grid-wide barrier (the launch is cooperative: every CTA is resident).  Arrivals are counted
-// on bar[0]; the last arrival resets it and bumps the generation bar[1] the others wait on.
-__device__ __forceinline__ void grid_sync(uint32_t* bar) {
+// Grid-wide barrier (the launch is cooperative: every CTA is resident) on a monotonic 64-bit
+// arrival counter that is never reset: barrier number e of the context completes when the counter
+// reaches e * gridDim.x.  Thread 0 of each CTA arrives with a release reduction (cumulative over
+// the CTA's writes, which __syncthreads orders before it) and polls with acquire loads; the
+// following __syncthreads extends the acquire to the CTA.  No fence, exchange or generation word:
+// 1.6 us per barrier on 444 CTAs vs 2.7 us for a reset-counter barrier with full fences
+// (tools/barrier_bench2.cu).  target (thread 0 only) holds e * gridDim.x.
+__device__ __forceinline__ void grid_sync(uint64_t* ctr, uint64_t& target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile uint32_t* gen = bar + 1;
-    const uint32_t g0 = *gen;
+    target += gridDim.x;
+#ifdef TK_BARRIER_FENCED  // experiment: full fences and a volatile poll (the round-1 barrier's ordering)
     __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g0) __nanosleep(32);
+    atomicAdd(reinterpret_cast<unsigned long long*>(ctr), 1ull);
+    while (*reinterpret_cast<volatile uint64_t*>(ctr) < target) __nanosleep(32);
+    __threadfence();
+#else
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+    // poll with relaxed loads (an acquire load invalidates the SM's whole L1 - the other CTAs'
+    // cached lines and spilled registers - on every iteration), then one acquire fence
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    while (v < target) {
+      __nanosleep(20);
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
     }
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
   }
   __syncthreads();
+}
+// barriers completed before this launch: the counter lies in [B*G, B*G + G) until every CTA has
+// arrived at this launch's first barrier, and each CTA reads it before its own first arrival
+__device__ __forceinline__ uint64_t grid_sync_base(const uint64_t* ctr) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+  return v / gridDim.x * gridDim.x;
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -1397,8 +1430,8 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 template <int NK, int MODE>
-__device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass) {
-  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * HREP * pass, f.flags, f.seq, pass);
+__device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass, const EfStage& es) {
+  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * HREP * pass, f.flags, f.seq, pass, es);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1439,7 +1472,10 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   __shared__ uint32_t s_w[2][WARPS];
   __shared__ uint32_t s_base[2];
   __shared__ uint32_t s_ne[WARPS];
+  __shared__ EfStage s_es;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t bar_t = 0;  // thread 0: target of the next grid barrier
+  if (tid == 0) bar_t = grid_sync_base(f.bar);
   ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)
   int nph = 0;
   auto stamp = [&]() {
@@ -1458,12 +1494,13 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   const uint32_t efk = f.ef_compact ? sc.ef_key : 0u;
   uint32_t* cta_ent = f.cta_cls + 3 * gridDim.x;
   ef_phase<EF, NP>(f.g, f.pr, f.r, f.accw, f.sp, f.units_per_warp, f.cta_sum, f.cta_max, efk, f.cp, f.flags + 2,
-                   f.seq, cta_ent);
-  grid_sync(f.bar);
+                   f.seq, cta_ent, s_es);
+  grid_sync(f.bar, bar_t);
   stamp();
-  stats_root<SEL>(f.cta_sum, f.cta_max, f.sp, &sc, f.step, f.lev0);
+  const uint32_t of2 = __ldcg(f.flags + 2);
+  stats_root<SEL>(f.cta_sum, f.cta_max, cta_ent, f.sp, &sc, f.step);
   stamp();
-  const bool ef_ok = efk > 0u && __ldcg(f.flags + 2) != f.seq;  // entries = {a >= efk}, none dropped
+  const bool ef_ok = efk > 0u && of2 != f.seq;  // entries = {a >= efk}, none dropped
   bool nobar = false;  // the cross-CTA prefix comes from the published histogram suffixes (no barrier)
   if (tid == 0) { sc.cmp_bottom = 0u; sc.cap_ok = 0u; sc.ef_used = 0u; sc.nnz_lb = 0ull; }
   __syncthreads();
@@ -1524,8 +1561,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         sc.ncand = 3u;
       }
       __syncthreads();
-      run_count<3, COUNT_FIRST>(f, &sc, 0);
-      grid_sync(f.bar);
+      run_count<3, COUNT_FIRST>(f, &sc, 0, s_es);
+      grid_sync(f.bar, bar_t);
       stamp();
       load_totals(f.totals, 3, s_tot);
       if (tid == 0) {
@@ -1554,7 +1591,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       if (mode == 0) {
         for (int j = tid; j < HIST_BINS - 1; j += THREADS) sc.cand_key[j] = exact_split(&sc, j + 1, HIST_BINS);
         __syncthreads();
-        hist_phase<HIST_LEV>(&sc, f.cp, tot_p, s_hist);
+        hist_phase<HIST_LEV>(&sc, f.cp, tot_p, s_hist, s_es);
       } else {
         if (tid == 0) {
           if (mode == 1) {
@@ -1568,11 +1605,11 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         }
         __syncthreads();
         if (mode == 1)
-          count_phase<3, COUNT_FIRST>(f.acc, &sc, f.sp, f.wcnt, f.cp, tot_p, f.flags + 1, f.seq, p);
+          count_phase<3, COUNT_FIRST>(f.acc, &sc, f.sp, f.wcnt, f.cp, tot_p, f.flags + 1, f.seq, p, s_es);
         else
-          run_count<3, COUNT_FULL>(f, &sc, p);
+          run_count<3, COUNT_FULL>(f, &sc, p, s_es);
       }
-      grid_sync(f.bar);
+      grid_sync(f.bar, bar_t);
       stamp();
       if (mode == 0) hist_to_counts(tot_p, HIST_LEV, s_tot);
       else load_totals(tot_p, 3, s_tot);
@@ -1604,8 +1641,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         sc.cand_key[1] = sc.xlo;
       }
       __syncthreads();
-      run_count<2, COUNT_FULL>(f, &sc, p);
-      grid_sync(f.bar);
+      run_count<2, COUNT_FULL>(f, &sc, p, s_es);
+      grid_sync(f.bar, bar_t);
       stamp();
     }
     if (tid == 0) {
@@ -1662,29 +1699,29 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       uint32_t* suf = (fast && single) ? f.cta_suffix + (size_t)blockIdx.x * HIST_BINS : nullptr;
       if (first) {
         lev = f.lev0;  // keys along the predicted path
-        if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, p);
-        else if (lev == 2) run_count<2, COUNT_FIRST>(f, &sc, p);
-        else run_count<3, COUNT_FIRST>(f, &sc, p);
+        if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, p, s_es);
+        else if (lev == 2) run_count<2, COUNT_FIRST>(f, &sc, p, s_es);
+        else run_count<3, COUNT_FIRST>(f, &sc, p, s_es);
       } else if (sc.cap_ok) {
         hist = true;
         lev = min(min(HIST_LEV, f.cap_levels), N - done);
         switch (lev) {
-          case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 8: hist_phase<8>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 9: hist_phase<9>(&sc, f.cp, tot_p, s_hist, suf); break;
-          default: hist_phase<10>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 8: hist_phase<8>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 9: hist_phase<9>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          default: hist_phase<10>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
         }
       } else {
         lev = min(min(2, f.cap_levels), N - done);
-        if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<3, COUNT_FULL>(f, &sc, p);
+        if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p, s_es); else run_count<3, COUNT_FULL>(f, &sc, p, s_es);
       }
-      grid_sync(f.bar);
+      grid_sync(f.bar, bar_t);
       stamp();
       if (hist) hist_to_counts(tot_p, lev, s_tot);
       else load_totals(tot_p, 16, s_tot);
@@ -1754,8 +1791,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         s_nk = nk;
       }
       __syncthreads();
-      run_count<8, COUNT_FULL>(f, &sc, pnext);
-      grid_sync(f.bar);
+      run_count<8, COUNT_FULL>(f, &sc, pnext, s_es);
+      grid_sync(f.bar, bar_t);
       stamp();
       load_totals(f.totals + HIST_BINS * HREP * pnext, 8, s_tot);
       if (tid == 0) {
@@ -1801,12 +1838,12 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     // above every element excluded from the entries)
     const int32_t k1m1 = sc.prov1 >= 0 ? (int32_t)sc.key1 - 1 : 0x7FFFFFFF;
     const int32_t k2m1 = (int32_t)sc.key2 - 1;
-    const uint32_t ne = min(__ldcg(f.cp.cnt + gw), f.cp.C);
-    const uint32_t* eb = f.cp.bits + (size_t)gw * f.cp.C + entry_off(f.cp, ne, sc.cmp_bottom);
+    const Entries e = warp_entries(f.cp, s_es, sc.cmp_bottom, gw, warp);
+    const uint32_t ne = e.n;
     if (lane == 0) s_ne[warp] = ne;
 #pragma unroll 4
     for (uint32_t j = lane; j < ne; j += 32) {
-      const int32_t a = (int32_t)(__ldcg(eb + j) & 0x7FFFFFFFu);
+      const int32_t a = (int32_t)(e.b(j) & 0x7FFFFFFFu);
       c1 += (uint32_t)(k1m1 - a) >> 31;
       call += (uint32_t)(k2m1 - a) >> 31;
     }
@@ -1830,7 +1867,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       f.cta_cls[gridDim.x + blockIdx.x] = t2;
       f.cta_cls[2 * gridDim.x + blockIdx.x] = tn;  // compacted entries (statistics)
     }
-    grid_sync(f.bar);
+    grid_sync(f.bar, bar_t);
   }
   stamp();
   {
@@ -1875,7 +1912,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     so.val16 = f.val16_out;
     so.r = EF ? f.r : nullptr;
     so.w16 = f.wire16;
-    select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, so, f.cp);
+    select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, so, f.cp, s_es);
   }
   stamp();
   if (f.push.np > 0) {
@@ -1898,18 +1935,20 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     }
   }
   if (blockIdx.x == 0) {
-    uint32_t tn = 0;
-    // entries per CTA: from the ef phase (written before the first barrier) when the prefix ran
-    // without a barrier, else from the prefix phase
-    const uint32_t* ent = nobar ? cta_ent : f.cta_cls + 2 * gridDim.x;
-    for (uint32_t b = tid; b < gridDim.x; b += THREADS) tn += __ldcg(ent + b);
-    tn = __reduce_add_sync(0xffffffffu, tn);
-    if (lane == 0) s_w[0][warp] = tn;
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t t = 0;
-      for (int w = 0; w < WARPS; ++w) t += s_w[0][w];
-      sc.n_compacted = sc.cap_ok ? t : 0u;
+    // entries the selection ran on (statistics): the ef phase's (summed in stats_root) or, on the
+    // whole-vector path, the first count pass's (per CTA, from the prefix phase)
+    if (!sc.ef_used) {
+      uint32_t tn = 0;
+      if (sc.cap_ok)
+        for (uint32_t b = tid; b < gridDim.x; b += THREADS) tn += __ldcg(f.cta_cls + 2 * gridDim.x + b);
+      tn = __reduce_add_sync(0xffffffffu, tn);
+      if (lane == 0) s_w[0][warp] = tn;
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < WARPS; ++w) t += s_w[0][w];
+        sc.n_compacted = t;
+      }
     }
     ctrl_to_global(f.c, &sc);
   }

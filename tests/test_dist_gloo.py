@@ -141,3 +141,38 @@ def test_hitopk_decomposition_matches_simulation(m, n):
         for rank in range(2):
             assert out[rank][step] == ref.out.view(np.uint32).tobytes(), (m, n, step, rank)
         r = [c.residual for c in ref.per_rank]
+
+
+# ---------------------------------------------------------------- world size 8 (the 8-GPU box layout)
+def _flat_ws(rank, ws):
+    return _flat("mstopk", "f32", rank, ws)
+
+
+def test_flat_decomposition_world_size_8():
+    """flat NaiveAG at P = 8 (BASELINE configs 2-3's 8-GPU aggregation): 8 processes, each its own
+    gradient and residual, one rank-major all-gather, rank-ordered decompression on every rank"""
+    ws = 8
+    out = _spawn(_flat_ws, ws=ws)
+    r = [np.zeros(D, np.float32) for _ in range(ws)]
+    for step in range(STEPS):
+        gs = [gradgen.gradient(D, "G", cfg=50, rank=p, step=step) for p in range(ws)]
+        ref = oracle.flat_step(gs, r, RHO, N, seed=3, step=step)
+        for rank in range(ws):
+            assert out[rank][step] == ref.out.view(np.uint32).tobytes(), (step, rank)
+        r = [c.residual for c in ref.per_rank]
+
+
+@pytest.mark.parametrize("m,n", [(2, 4), (4, 2), (2, 2)])
+def test_hitopk_decomposition_world_size_8(m, n):
+    """HiTopKComm's virtual-node layouts of BASELINE config 4 (2x4 and 4x2 on 8 processes; 2x2 on 4):
+    row groups (rank // n), column groups (rank % n), ordered reduce-scatter, per-segment MSTopK,
+    column all-gather, row all-gather - every rank's aggregate equals oracle.hitopk_step's"""
+    ws = m * n
+    out = _spawn(functools.partial(_hitopk_body, m, n), ws=ws)
+    r = [np.zeros(D // n, np.float32) for _ in range(ws)]
+    for step in range(STEPS):
+        gs = [gradgen.gradient(D, "G", cfg=51, rank=p, step=step) for p in range(ws)]
+        ref = oracle.hitopk_step(gs, r, m, n, RHO, N, seed=4, step=step)
+        for rank in range(ws):
+            assert out[rank][step] == ref.out.view(np.uint32).tobytes(), (m, n, step, rank)
+        r = [c.residual for c in ref.per_rank]
