@@ -146,6 +146,9 @@ SearchParams search_params(const tk_ctx* c) {
 template <int SEL>
 const void* compress_kernel_sel(bool ef, int np) {
   // NP: the number of gradient sources summed in the ef phase (0 = one plain vector)
+#ifdef TK_ANALYZE  // register / spill analysis of one instantiation only (never a product build)
+  return (ef && np == 0 && SEL == SEL_MSTOPK) ? reinterpret_cast<const void*>(&k_compress<true, 0, SEL_MSTOPK>) : nullptr;
+#endif
   switch ((ef ? 100 : 0) + np) {
     case 100: return reinterpret_cast<const void*>(&k_compress<true, 0, SEL>);
     case 102: return reinterpret_cast<const void*>(&k_compress<true, 2, SEL>);

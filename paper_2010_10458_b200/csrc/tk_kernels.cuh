@@ -277,7 +277,7 @@ __device__ __forceinline__ void prose_advance(double& t, double& lo, double& hi,
 // Computed by the CTA's threads in parallel (candidate m-1 by thread m-1); the caller
 // synchronises the CTA before and after.
 template <int SEL>
-__device__ void make_candidates_par(Ctrl* c, int lev) {
+__device__ __forceinline__ void make_candidates_par(Ctrl* c, int lev) {
   const int T = (1 << lev) - 1;  // <= 1023
   if constexpr (SEL == SEL_PROSE) {
     for (int m = (int)threadIdx.x + 1; m <= T; m += THREADS) {
@@ -307,7 +307,7 @@ __device__ void make_candidates_par(Ctrl* c, int lev) {
 
 // Replay lev levels of Alg. 1 l.8-23 on the candidates' exact counts.
 template <int SEL>
-__device__ int replay_levels(Ctrl* c, const uint32_t* totals, int max_lev, int pass, uint64_t k) {
+__device__ __forceinline__ int replay_levels(Ctrl* c, const uint32_t* totals, int max_lev, int pass, uint64_t k) {
   // Alg. 1 l.8-23, one level at a time: the level's trial (Alg. 1: ratio l + (r-l)/2, exact, Q5;
   // prose: the state's next threshold) is looked up among the counted candidates; the replay
   // stops at the first level whose threshold was not counted (speculative candidate sets).
@@ -370,7 +370,7 @@ __device__ int replay_levels(Ctrl* c, const uint32_t* totals, int max_lev, int p
 // for the prose search).  When the data take that path, one read of the vector resolves lev
 // levels with lev keys; otherwise it resolves at least one.
 template <int SEL>
-__device__ void make_candidates_path(Ctrl* c, int lev, double target) {
+__device__ __forceinline__ void make_candidates_path(Ctrl* c, int lev, double target) {
   if constexpr (SEL == SEL_PROSE) {
     double t = c->pt, lo = c->lo, hi = c->hi;
     uint32_t ls = c->lo_set, hs = c->hi_set;
@@ -403,7 +403,7 @@ __device__ __forceinline__ bool bracket_low_at_least(const Ctrl* c, double x) {
 }
 
 // Alg. 1 l.27 window: R = len(iota2) - (k - k1) + 1 >= 1 (Q8, Q9); rand uniform on [0, R).
-__device__ void finish_window(Ctrl* c, const SearchParams& sp) {
+__device__ __forceinline__ void finish_window(Ctrl* c, const SearchParams& sp) {
   const uint64_t k1 = c->k1;
   const uint64_t cnt2 = (c->prov2 >= 0) ? (uint64_t)c->k2 : sp.n;  // count(a >= thres2)
   const uint64_t len2 = cnt2 - k1;
@@ -473,7 +473,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 // the previous compression ended in; the compaction key is the highest of them at or below that
 // bracket (any choice is exact; a good one keeps few elements).  One thread.
 template <int SEL>
-__device__ void first_pass_candidates(Ctrl* sc, int first_levels) {
+__device__ __forceinline__ void first_pass_candidates(Ctrl* sc, int first_levels) {
   make_candidates_path<SEL>(sc, first_levels, sc->prev_lo);
   int ms = 0;
   for (int q = 1; q < (int)sc->ncand; ++q)
@@ -511,7 +511,7 @@ __device__ __forceinline__ void search_reset(Ctrl* c, uint64_t n) {
 }
 
 template <int SEL>
-__device__ void stats_finalize(Ctrl* c, const SearchParams& sp, double S, uint32_t m, uint64_t step) {
+__device__ __forceinline__ void stats_finalize(Ctrl* c, const SearchParams& sp, double S, uint32_t m, uint64_t step) {
   // the previous call's final bracket low end predicts this call's (prose: 0 when never set)
   c->prev_lo = (SEL == SEL_PROSE && !c->lo_set) ? 0.0 : c->lo;
   c->abar = __ddiv_rn(S, (double)sp.n);                 // Alg. 1 l.2
@@ -574,36 +574,34 @@ struct EfStage {
   uint32_t n[WARPS];         // entries of the warp
   uint32_t in_smem[WARPS];   // 1: all of them are in si/sb (none spilled)
 };
+// one per CTA of k_compress (file scope: its address is a constant, so no register holds it)
+__shared__ EfStage g_es;
 
-// A warp's compacted entries, wherever they are (ascending index order)
+// A warp's compacted entries, wherever they are (ascending index order): generic pointers into the
+// warp's shared-memory staging buffer or its global region.  Plain (generic) loads are safe for the
+// global case too: a warp only ever reads entries it wrote itself earlier in the same launch (same
+// SM, whose L1 never holds a stale copy of its own stores).
 struct Entries {
   const uint32_t* idx;
   const uint32_t* bits;
   uint32_t n;
-  bool smem;
-  __device__ __forceinline__ uint32_t b(uint32_t j) const { return smem ? bits[j] : __ldcg(bits + j); }
-  __device__ __forceinline__ uint32_t i(uint32_t j) const { return smem ? idx[j] : __ldcg(idx + j); }
-  __device__ __forceinline__ uint4 b4(uint32_t j) const {
-    return smem ? make_uint4(bits[j], bits[j + 1], bits[j + 2], bits[j + 3]) : ldcg4(bits + j);
-  }
-  __device__ __forceinline__ uint4 i4(uint32_t j) const {
-    return smem ? make_uint4(idx[j], idx[j + 1], idx[j + 2], idx[j + 3]) : ldcg4(idx + j);
-  }
+  __device__ __forceinline__ uint32_t b(uint32_t j) const { return bits[j]; }
+  __device__ __forceinline__ uint32_t i(uint32_t j) const { return idx[j]; }
+  __device__ __forceinline__ uint4 b4(uint32_t j) const { return make_uint4(bits[j], bits[j + 1], bits[j + 2], bits[j + 3]); }
+  __device__ __forceinline__ uint4 i4(uint32_t j) const { return make_uint4(idx[j], idx[j + 1], idx[j + 2], idx[j + 3]); }
 };
-__device__ __forceinline__ Entries warp_entries(const Compact& cp, const EfStage& es, uint32_t cmp_bottom, uint32_t gw,
-                                                int warp) {
+__device__ __forceinline__ Entries warp_entries(const Compact& cp, uint32_t cmp_bottom, uint32_t gw, int warp) {
+  const EfStage& es = g_es;
   Entries e;
   if (cmp_bottom && es.in_smem[warp]) {
     e.idx = es.si[warp];
     e.bits = es.sb[warp];
     e.n = es.n[warp];
-    e.smem = true;
   } else {
     e.n = min(__ldcg(cp.cnt + gw), cp.C);
     const uint32_t off = entry_off(cp, e.n, cmp_bottom);
     e.idx = cp.idx + (size_t)gw * cp.C + off;
     e.bits = cp.bits + (size_t)gw * cp.C + off;
-    e.smem = false;
   }
   return e;
 }
@@ -633,7 +631,8 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
                                          float* accw, const SearchParams& sp, uint32_t units_per_warp,
                                          double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max,
                                          uint32_t ckey, const Compact cp, uint32_t* overflow, uint32_t seq,
-                                         uint32_t* __restrict__ cta_ent, EfStage& es) {
+                                         uint32_t* __restrict__ cta_ent) {
+  EfStage& es = g_es;
   constexpr bool STORE = EF || NP > 0;
   __shared__ double s_ws[WARPS];
   __shared__ uint32_t s_wm[WARPS];
@@ -798,7 +797,7 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
 // the CTA partials zero-padded to Lp = 2^j >= THREADS leaves (extra zero leaves never change a
 // pairwise sum of non-negatives, Q3), then a-bar, u and the first pass's candidates.
 template <int SEL>
-__device__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* __restrict__ cta_max,
+__device__ __forceinline__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* __restrict__ cta_max,
                            const uint32_t* __restrict__ cta_ent, const SearchParams& sp, Ctrl* sc, uint64_t step) {
   __shared__ double s_v[THREADS];
   __shared__ uint32_t s_m[WARPS], s_n[WARPS];
@@ -867,7 +866,7 @@ enum { COUNT_FIRST = 0, COUNT_CAP = 1, COUNT_FULL = 2 };
 template <int NK, int MODE>
 __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const Ctrl* sc, const SearchParams sp,
                                             uint32_t* __restrict__ wcnt, const Compact cp, uint32_t* totals,
-                                            uint32_t* overflow, uint32_t seq, int pass, const EfStage& es) {
+                                            uint32_t* overflow, uint32_t seq, int pass) {
   constexpr int T = NK;  // keys counted in this pass
   __shared__ uint32_t s_cnt[WARPS][16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -888,7 +887,7 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
     for (int s = 0; s < T; ++s) cnt[s] += (uint32_t)(km1[s] - a) >> 31;
   };
   if (MODE == COUNT_CAP) {
-    const Entries e = warp_entries(cp, es, sc->cmp_bottom, gw, warp);
+    const Entries e = warp_entries(cp, sc->cmp_bottom, gw, warp);
     const uint32_t ne = e.n;
     // this warp's entry loads in flight together (4 x 128 entries per iteration)
     for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
@@ -1046,7 +1045,7 @@ struct HistSmem {
 // grid barrier (#entries of CTA c at or above candidate s = S_c[s + 1]).
 template <int LEV>
 __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uint32_t* ghist, HistSmem& hs,
-                                           const EfStage& es, uint32_t* suf = nullptr) {
+                                           uint32_t* suf = nullptr) {
   constexpr int NB = 1 << LEV;
   const int32_t* s_key = reinterpret_cast<const int32_t*>(sc->cand_key);  // sorted, in shared memory
   uint32_t* s_h = hs.h;
@@ -1054,7 +1053,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
   for (int i = threadIdx.x; i < NB; i += THREADS) s_h[i] = 0u;
   __syncthreads();
   const uint32_t gw = blockIdx.x * WARPS + warp;
-  const Entries e = warp_entries(cp, es, sc->cmp_bottom, gw, warp);
+  const Entries e = warp_entries(cp, sc->cmp_bottom, gw, warp);
   const uint32_t ne = e.n;
   auto add = [&](uint32_t bits) {
     const int32_t a = (int32_t)(bits & 0x7FFFFFFFu);
@@ -1177,7 +1176,7 @@ __device__ __forceinline__ void put_sel(const SelOut& o, uint32_t pos, uint32_t 
 
 __device__ __forceinline__ void select_phase(const float* __restrict__ acc, const Ctrl* c, const SearchParams sp,
                                           uint32_t c1, uint32_t c2, uint32_t b1, uint32_t b2, const SelOut& so,
-                                          const Compact cp, const EfStage& es) {
+                                          const Compact cp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint64_t lo = min(sp.n, (uint64_t)gw * sp.S);
@@ -1191,7 +1190,7 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
   if (c->cap_ok) {
     // ---- compacted entries of this warp (ascending index order): 128 per iteration, lane l
     // holds entries 4l..4l+3 of the group, so (lane, e) order is index order ----
-    const Entries en = warp_entries(cp, es, c->cmp_bottom, gw, warp);
+    const Entries en = warp_entries(cp, c->cmp_bottom, gw, warp);
     const uint32_t ne = en.n;
     for (uint32_t j0 = 0; j0 < ne; j0 += 128) {
       const uint32_t j = j0 + 4 * lane;
@@ -1430,8 +1429,8 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 template <int NK, int MODE>
-__device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass, const EfStage& es) {
-  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * HREP * pass, f.flags, f.seq, pass, es);
+__device__ __forceinline__ void run_count(const Fused& f, Ctrl* sc, int pass) {
+  count_phase<NK, MODE>(f.acc, sc, f.sp, f.wcnt, f.cp, f.totals + HIST_BINS * HREP * pass, f.flags, f.seq, pass);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1463,8 +1462,11 @@ __device__ __forceinline__ uint32_t exact_split(const Ctrl* c, uint32_t j, uint3
   return c->xlo + (uint32_t)((j * w + parts - 1) / parts);
 }
 
+#ifndef TK_MIN_BLOCKS
+#define TK_MIN_BLOCKS 3
+#endif
 template <bool EF, int NP, int SEL>
-__global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
+__global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   static_assert(SEL == SEL_MSTOPK || SEL == SEL_EXACT || SEL == SEL_PROSE, "selector");
   __shared__ Ctrl sc;
   __shared__ uint32_t s_tot[HIST_BINS];
@@ -1472,9 +1474,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   __shared__ uint32_t s_w[2][WARPS];
   __shared__ uint32_t s_base[2];
   __shared__ uint32_t s_ne[WARPS];
-  __shared__ EfStage s_es;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint64_t bar_t = 0;  // thread 0: target of the next grid barrier
+  __shared__ uint64_t bar_t;  // thread 0: target of the next grid barrier (shared: keeps it out of registers)
   if (tid == 0) bar_t = grid_sync_base(f.bar);
   ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)
   int nph = 0;
@@ -1494,7 +1495,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   const uint32_t efk = f.ef_compact ? sc.ef_key : 0u;
   uint32_t* cta_ent = f.cta_cls + 3 * gridDim.x;
   ef_phase<EF, NP>(f.g, f.pr, f.r, f.accw, f.sp, f.units_per_warp, f.cta_sum, f.cta_max, efk, f.cp, f.flags + 2,
-                   f.seq, cta_ent, s_es);
+                   f.seq, cta_ent);
   grid_sync(f.bar, bar_t);
   stamp();
   const uint32_t of2 = __ldcg(f.flags + 2);
@@ -1561,7 +1562,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         sc.ncand = 3u;
       }
       __syncthreads();
-      run_count<3, COUNT_FIRST>(f, &sc, 0, s_es);
+      run_count<3, COUNT_FIRST>(f, &sc, 0);
       grid_sync(f.bar, bar_t);
       stamp();
       load_totals(f.totals, 3, s_tot);
@@ -1591,7 +1592,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       if (mode == 0) {
         for (int j = tid; j < HIST_BINS - 1; j += THREADS) sc.cand_key[j] = exact_split(&sc, j + 1, HIST_BINS);
         __syncthreads();
-        hist_phase<HIST_LEV>(&sc, f.cp, tot_p, s_hist, s_es);
+        hist_phase<HIST_LEV>(&sc, f.cp, tot_p, s_hist);
       } else {
         if (tid == 0) {
           if (mode == 1) {
@@ -1605,9 +1606,9 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         }
         __syncthreads();
         if (mode == 1)
-          count_phase<3, COUNT_FIRST>(f.acc, &sc, f.sp, f.wcnt, f.cp, tot_p, f.flags + 1, f.seq, p, s_es);
+          count_phase<3, COUNT_FIRST>(f.acc, &sc, f.sp, f.wcnt, f.cp, tot_p, f.flags + 1, f.seq, p);
         else
-          run_count<3, COUNT_FULL>(f, &sc, p, s_es);
+          run_count<3, COUNT_FULL>(f, &sc, p);
       }
       grid_sync(f.bar, bar_t);
       stamp();
@@ -1641,7 +1642,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         sc.cand_key[1] = sc.xlo;
       }
       __syncthreads();
-      run_count<2, COUNT_FULL>(f, &sc, p, s_es);
+      run_count<2, COUNT_FULL>(f, &sc, p);
       grid_sync(f.bar, bar_t);
       stamp();
     }
@@ -1683,7 +1684,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
   const int N = (int)f.n_iters;
   const bool single = N <= min(HIST_LEV, f.cap_levels);  // the fast search resolves all N levels in one pass
   __shared__ int s_got;
-  auto search = [&](int p0, bool fast) -> int {
+  // the search (always inlined: a call would spill the whole kernel's live state)
+  auto search = [&](int p0, bool fast) __attribute__((always_inline)) -> int {
     int done = 0;
     int p = p0;
     if (fast) {
@@ -1699,27 +1701,27 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       uint32_t* suf = (fast && single) ? f.cta_suffix + (size_t)blockIdx.x * HIST_BINS : nullptr;
       if (first) {
         lev = f.lev0;  // keys along the predicted path
-        if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, p, s_es);
-        else if (lev == 2) run_count<2, COUNT_FIRST>(f, &sc, p, s_es);
-        else run_count<3, COUNT_FIRST>(f, &sc, p, s_es);
+        if (lev == 1) run_count<1, COUNT_FIRST>(f, &sc, p);
+        else if (lev == 2) run_count<2, COUNT_FIRST>(f, &sc, p);
+        else run_count<3, COUNT_FIRST>(f, &sc, p);
       } else if (sc.cap_ok) {
         hist = true;
         lev = min(min(HIST_LEV, f.cap_levels), N - done);
         switch (lev) {
-          case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          case 8: hist_phase<8>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          case 9: hist_phase<9>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
-          default: hist_phase<10>(&sc, f.cp, tot_p, s_hist, s_es, suf); break;
+          case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 8: hist_phase<8>(&sc, f.cp, tot_p, s_hist, suf); break;
+          case 9: hist_phase<9>(&sc, f.cp, tot_p, s_hist, suf); break;
+          default: hist_phase<10>(&sc, f.cp, tot_p, s_hist, suf); break;
         }
       } else {
         lev = min(min(2, f.cap_levels), N - done);
-        if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p, s_es); else run_count<3, COUNT_FULL>(f, &sc, p, s_es);
+        if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<3, COUNT_FULL>(f, &sc, p);
       }
       grid_sync(f.bar, bar_t);
       stamp();
@@ -1763,7 +1765,6 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     __syncthreads();
     ok = s_got != 0;
   }
-  nobar = ok && single;
   if (!ok) {
     if (tid == 0) {
       search_reset<SEL>(&sc, f.sp.n);
@@ -1775,6 +1776,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     __syncthreads();
     pnext = search(pnext, false);
   }
+  nobar = ok && single;
+#ifndef TK_NO_EXACT_COUNTS
   if (f.exact_counts) {
     // exact_trial_counts: the trials the fast search only knows as "nnz > k" (key below the
     // ef-phase key) are counted exactly, up to 8 per whole-vector pass, before the selection
@@ -1791,7 +1794,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
         s_nk = nk;
       }
       __syncthreads();
-      run_count<8, COUNT_FULL>(f, &sc, pnext, s_es);
+      run_count<8, COUNT_FULL>(f, &sc, pnext);
       grid_sync(f.bar, bar_t);
       stamp();
       load_totals(f.totals + HIST_BINS * HREP * pnext, 8, s_tot);
@@ -1805,6 +1808,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
       ++pnext;
     }
   }
+#endif
   if (tid == 0) {
     sc.ef_used = ok ? 1u : 0u;
     // next call's ef-phase compaction key: below this key2 by twice its last move plus a margin
@@ -1838,7 +1842,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     // above every element excluded from the entries)
     const int32_t k1m1 = sc.prov1 >= 0 ? (int32_t)sc.key1 - 1 : 0x7FFFFFFF;
     const int32_t k2m1 = (int32_t)sc.key2 - 1;
-    const Entries e = warp_entries(f.cp, s_es, sc.cmp_bottom, gw, warp);
+    const Entries e = warp_entries(f.cp, sc.cmp_bottom, gw, warp);
     const uint32_t ne = e.n;
     if (lane == 0) s_ne[warp] = ne;
 #pragma unroll 4
@@ -1912,7 +1916,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_compress(Fused f) {
     so.val16 = f.val16_out;
     so.r = EF ? f.r : nullptr;
     so.w16 = f.wire16;
-    select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, so, f.cp, s_es);
+    select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, so, f.cp);
   }
   stamp();
   if (f.push.np > 0) {
