@@ -37,6 +37,7 @@ struct tk_ctx {
   uint32_t grid = 0;                  // CTAs of the cooperative compression kernel
   uint32_t W = 0;                     // warp slabs
   uint64_t S = 0;                     // slab length
+  uint32_t R = 0;                     // runs of S elements (<= W; warp_run spreads them over the warps)
   uint32_t occ_dec = 1;               // resident decompression CTAs per SM
   uint32_t levels = 4, npass = 0;
   uint32_t debug_check = 0;           // cfg.check_selection: verify every selection on the device
@@ -137,6 +138,7 @@ SearchParams search_params(const tk_ctx* c) {
   sp.k = c->k;
   sp.W = c->W;
   sp.S = c->S;
+  sp.R = c->R;
   sp.rank = c->rank;
   sp.rand_mode = c->cfg.rand_mode;
   sp.seed = c->cfg.seed;
@@ -293,12 +295,14 @@ tk_status plan_launches(tk_ctx* c) {
   const uint64_t rounds = (L + ROUND - 1) / ROUND;
   // persistent cooperative grid: every CTA resident; no more CTAs than warp rounds of work
   c->grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sms * occ, (rounds + WARPS - 1) / WARPS));
+  c->grid = std::min<uint32_t>(c->grid, 4096);  // stats_root folds <= 4096 CTA partials
   c->W = c->grid * WARPS;
   uint64_t upw = 1;  // ef phase: aligned power-of-two run of units per warp covering the vector
   while ((uint64_t)c->W * upw < rounds) upw <<= 1;
   c->units_per_warp = (uint32_t)upw;
   c->S = upw * ROUND;  // count / select slabs = the ef phase's warp runs (acc is re-read from L2)
-  TK_TRY(dev_alloc(c, &c->cta_sum, c->grid));
+  c->R = (uint32_t)((rounds + upw - 1) / upw);
+  TK_TRY(dev_alloc(c, &c->cta_sum, c->grid));  // one partial sum per CTA
   TK_TRY(dev_alloc(c, &c->cta_max, c->grid));
   TK_TRY(dev_alloc(c, &c->cta_cls, 4 * (size_t)c->grid));
   TK_TRY(dev_alloc(c, &c->cta_suffix, (size_t)c->grid * HIST_BINS));
@@ -902,5 +906,12 @@ const char* tk_status_string(tk_status s) {
 }
 
 const char* tk_last_error(const tk_ctx* c) { return c ? c->err : "no context"; }
+
+#ifdef TK_PHASE_TRACE
+// experiment builds only (tools/trace_probe.py): the per-CTA phase timeline of the last k_compress
+tk_status tk_debug_trace(uint64_t* out /* host [2][32][2048] */) {
+  return cudaMemcpyFromSymbol(out, tk::g_trace, sizeof(tk::g_trace)) == cudaSuccess ? TK_OK : TK_ERR_CUDA;
+}
+#endif
 
 }  // extern "C"

@@ -16,6 +16,20 @@
 
 namespace tk {
 
+#ifdef TK_PHASE_TRACE  // experiment builds only: per-CTA %globaltimer at every phase stamp / barrier arrival
+__device__ uint64_t g_trace[2][32][2048];
+#define TK_TRACE(slot)                                                                                   \
+  do {                                                                                                   \
+    if (threadIdx.x == 0 && blockIdx.x < 2048) {                                                         \
+      uint64_t t_;                                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                             \
+      g_trace[0][(slot)][blockIdx.x] = t_;                                                               \
+    }                                                                                                    \
+  } while (0)
+#else
+#define TK_TRACE(slot) do { } while (0)
+#endif
+
 constexpr int TILE = 4096;          // elements per pairwise-sum tile (power of two, Q3) / output tile
 constexpr int THREADS = 256;        // 8 warps per CTA
 constexpr int WARPS = THREADS / 32;
@@ -112,11 +126,20 @@ struct SearchParams {
   uint64_t n;        // vector length MSTopK runs on (d, or d/n for HiTopKComm)
   uint64_t k;        // number of elements to select
   uint32_t W;        // warp slabs (= gridDim.x * WARPS of the count / select launches)
-  uint64_t S;        // slab length
+  uint64_t S;        // slab length (one run of units_per_warp 512-element units)
+  uint32_t R;        // runs: ceil(n / S) <= W
   uint32_t rank;
   uint32_t rand_mode;
   uint64_t seed;
 };
+
+// Warp -> run map: run j (elements [j*S, (j+1)*S)) belongs to warp j; the W - R warps past the end
+// are idle.  (Spreading the idle warps evenly over the CTAs was measured: it moves the last CTA's
+// end of the EF pass by only 0.5 us - the spread comes from the memory system, not the partition -
+// and it breaks the CTA-level fold of the canonical tree, which then costs more at the root.)
+__device__ __forceinline__ int32_t warp_run_of(const SearchParams& sp, uint32_t gw) {
+  return gw < sp.R ? (int32_t)gw : -1;
+}
 
 // Compacted entries of the first count pass: warp w keeps, in ascending index order, every
 // element of its slab with |acc| >= the compaction key, at the top of its region
@@ -573,9 +596,16 @@ struct EfStage {
   uint32_t sb[WARPS][SCAP];  // bits of acc
   uint32_t n[WARPS];         // entries of the warp
   uint32_t in_smem[WARPS];   // 1: all of them are in si/sb (none spilled)
+  int32_t run[WARPS];        // the warp's run (warp_run_of), -1: idle
 };
 // one per CTA of k_compress (file scope: its address is a constant, so no register holds it)
 __shared__ EfStage g_es;
+// this warp's slab [lo, hi) of the count and selection phases (empty for an idle warp)
+__device__ __forceinline__ void warp_slab(const SearchParams& sp, int warp, uint64_t& lo, uint64_t& hi) {
+  const int32_t j = g_es.run[warp];
+  lo = j < 0 ? sp.n : min(sp.n, (uint64_t)j * sp.S);
+  hi = j < 0 ? sp.n : min(sp.n, lo + sp.S);
+}
 
 // A warp's compacted entries, wherever they are (ascending index order): generic pointers into the
 // warp's shared-memory staging buffer or its global region.  Plain (generic) loads are safe for the
@@ -629,7 +659,7 @@ __device__ __forceinline__ uint32_t quad_max_bits(float4 v) {
 template <bool EF, int NP>
 __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peers& pr, const float* r,
                                          float* accw, const SearchParams& sp, uint32_t units_per_warp,
-                                         double* __restrict__ cta_sum, uint32_t* __restrict__ cta_max,
+                                         double* __restrict__ run_sum, uint32_t* __restrict__ cta_max,
                                          uint32_t ckey, const Compact cp, uint32_t* overflow, uint32_t seq,
                                          uint32_t* __restrict__ cta_ent) {
   EfStage& es = g_es;
@@ -639,7 +669,9 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t n = sp.n;
   const uint32_t gw = blockIdx.x * WARPS + warp;
-  const uint64_t u0 = (uint64_t)gw * units_per_warp;
+  const int32_t run = es.run[warp];
+  const uint64_t u0 = run < 0 ? 0 : (uint64_t)run * units_per_warp;
+  const uint32_t nunits = run < 0 ? 0u : units_per_warp;
   const bool cmp_on = ckey > 0u;
   const int32_t ckm1 = (int32_t)ckey - 1;
   uint32_t staged = 0, flushed = 0;  // warp-uniform: entries in the staging buffer / spilled
@@ -659,8 +691,9 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
     __syncwarp();
   };
   double stk[24];
+  stk[0] = 0.0;
   uint32_t mx = 0;
-  for (uint32_t i = 0; i < units_per_warp; ++i) {
+  for (uint32_t i = 0; i < nunits; ++i) {
     const uint64_t u = u0 + i;
     const uint64_t base = u * ROUND + 4 * lane;
     float4 acc[4];
@@ -677,7 +710,7 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
       }
       if (STORE) {
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) *reinterpret_cast<float4*>(accw + base + ch * 128) = acc[ch];
+        for (int ch = 0; ch < 4; ++ch) __stcs(reinterpret_cast<float4*>(accw + base + ch * 128), acc[ch]);
       }
     } else {
 #pragma unroll
@@ -769,7 +802,7 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   while ((1u << top) < units_per_warp) ++top;
   mx = __reduce_max_sync(0xffffffffu, mx);
   if (lane == 0) {
-    s_ws[warp] = stk[top];
+    s_ws[warp] = run >= 0 ? stk[top] : 0.0;  // this run's aligned subtree of the canonical tree
     s_wm[warp] = mx;
     es.n[warp] = cmp_on ? ncomp : 0u;
     es.in_smem[warp] = in_smem ? 1u : 0u;
@@ -784,7 +817,8 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) te += es.n[w];
     cta_ent[blockIdx.x] = te;
-    cta_sum[blockIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(s_ws[0], s_ws[1]), __dadd_rn(s_ws[2], s_ws[3])),
+    // the CTA's 8 runs form an aligned subtree (the CTA owns runs [8b, 8b + 8))
+    run_sum[blockIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(s_ws[0], s_ws[1]), __dadd_rn(s_ws[2], s_ws[3])),
                                     __dadd_rn(__dadd_rn(s_ws[4], s_ws[5]), __dadd_rn(s_ws[6], s_ws[7])));
     uint32_t m = s_wm[0];
 #pragma unroll
@@ -797,54 +831,51 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
 // the CTA partials zero-padded to Lp = 2^j >= THREADS leaves (extra zero leaves never change a
 // pairwise sum of non-negatives, Q3), then a-bar, u and the first pass's candidates.
 template <int SEL>
-__device__ __forceinline__ void stats_root(const double* __restrict__ cta_sum, const uint32_t* __restrict__ cta_max,
-                           const uint32_t* __restrict__ cta_ent, const SearchParams& sp, Ctrl* sc, uint64_t step) {
-  __shared__ double s_v[THREADS];
+__device__ __forceinline__ void stats_root(const double* __restrict__ run_sum, const uint32_t* __restrict__ cta_max,
+                                           const uint32_t* __restrict__ cta_ent, const SearchParams& sp, Ctrl* sc,
+                                           uint64_t step) {
+  // the CTA partials, zero-padded to Rp = 2^j >= THREADS leaves (extra zero leaves never change a
+  // pairwise sum of non-negatives, Q3): thread t folds its G consecutive leaves (binary-counter
+  // stack), the warp's 32 threads by xor shuffles, the 8 warps in thread 0 - the same pairs as the
+  // recursive definition
+  __shared__ double s_v[WARPS];
   __shared__ uint32_t s_m[WARPS], s_n[WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t Lp = THREADS;
-  while (Lp < gridDim.x) Lp <<= 1;
-  const uint32_t G = Lp / THREADS;  // <= 8 for grids up to 2048 CTAs
-  double leaf[8];
+  uint32_t Rp = THREADS;
+  while (Rp < gridDim.x) Rp <<= 1;
+  const uint32_t G = Rp / THREADS;  // leaves (CTA partials) per thread
   uint32_t m2 = 0, ne = 0;
+  for (uint32_t b = tid; b < gridDim.x; b += THREADS) {
+    m2 = max(m2, __ldcg(cta_max + b));
+    ne += __ldcg(cta_ent + b);
+  }
+  // G <= 16 consecutive leaves per thread (grids up to 4096 CTAs), loaded together, then
+  // folded pairwise (G is a power of two: the loops below visit exactly the pairs of a G-leaf tree)
+  double lv[16];
 #pragma unroll
-  for (uint32_t q = 0; q < 8; ++q) {
+  for (uint32_t q = 0; q < 16; ++q) {
     const uint32_t li = tid * G + q;
-    leaf[q] = 0.0;
-    if (q < G && li < gridDim.x) {
-      leaf[q] = __ldcg(cta_sum + li);
-      m2 = max(m2, __ldcg(cta_max + li));
-      ne += __ldcg(cta_ent + li);
-    }
+    lv[q] = (q < G && li < gridDim.x) ? __ldcg(run_sum + li) : 0.0;
   }
-  double st2[4];
 #pragma unroll
-  for (uint32_t q = 0; q < 8; ++q) {
-    if (q < G) {
-      double v = leaf[q];
-      int lvl = 0;
-      for (uint32_t cnt = q; cnt & 1u; cnt >>= 1) v = __dadd_rn(st2[lvl++], v);
-      st2[lvl] = v;
-    }
-  }
-  int top2 = 0;
-  while ((1u << top2) < G) ++top2;
-  s_v[tid] = st2[top2];
+  for (uint32_t w = 1; w < 16; w <<= 1)
+#pragma unroll
+    for (uint32_t q = 0; q < 16; q += 2 * w)
+      if (w < G) lv[q] = __dadd_rn(lv[q], lv[q + w]);
+  double v = lv[0];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
   m2 = __reduce_max_sync(0xffffffffu, m2);
   ne = __reduce_add_sync(0xffffffffu, ne);
-  if (lane == 0) { s_m[warp] = m2; s_n[warp] = ne; }
+  if (lane == 0) { s_v[warp] = v; s_m[warp] = m2; s_n[warp] = ne; }
   __syncthreads();
-  for (int h = THREADS / 2; h >= 1; h >>= 1) {
-    double v = 0.0;
-    if (tid < h) v = __dadd_rn(s_v[2 * tid], s_v[2 * tid + 1]);
-    __syncthreads();
-    if (tid < h) s_v[tid] = v;
-    __syncthreads();
-  }
   if (tid == 0) {
+    static_assert(WARPS == 8, "the CTA-level fold below is written for 8 warps");
+    const double S = __dadd_rn(__dadd_rn(__dadd_rn(s_v[0], s_v[1]), __dadd_rn(s_v[2], s_v[3])),
+                               __dadd_rn(__dadd_rn(s_v[4], s_v[5]), __dadd_rn(s_v[6], s_v[7])));
     uint32_t m = s_m[0], t = s_n[0];
     for (int w = 1; w < WARPS; ++w) { m = max(m, s_m[w]); t += s_n[w]; }
-    stats_finalize<SEL>(sc, sp, s_v[0], m, step);
+    stats_finalize<SEL>(sc, sp, S, m, step);
     sc->n_compacted = t;  // entries the ef phase kept (statistics)
   }
   __syncthreads();
@@ -875,8 +906,8 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
   for (int s = 0; s < T; ++s) km1[s] = (int32_t)sc->cand_key[s] - 1;
   const int32_t kcmp1 = (int32_t)sc->cmp_key - 1;
   const uint32_t gw = blockIdx.x * WARPS + warp;
-  const uint64_t lo = min(sp.n, (uint64_t)gw * sp.S);
-  const uint64_t hi = min(sp.n, lo + sp.S);
+  uint64_t lo, hi;
+  warp_slab(sp, warp, lo, hi);
   const uint32_t* a32 = reinterpret_cast<const uint32_t*>(acc);
   uint32_t cnt[T];
 #pragma unroll
@@ -888,26 +919,8 @@ __device__ __forceinline__ void count_phase(const float* __restrict__ acc, const
   };
   if (MODE == COUNT_CAP) {
     const Entries e = warp_entries(cp, sc->cmp_bottom, gw, warp);
-    const uint32_t ne = e.n;
-    // this warp's entry loads in flight together (4 x 128 entries per iteration)
-    for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
-      uint4 q[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t j = j0 + u * 128 + 4 * lane;
-        q[u] = make_uint4(0u, 0u, 0u, 0u);
-        if (j + 4 <= ne) q[u] = e.b4(j);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t j = j0 + u * 128 + 4 * lane;
-        if (j + 4 <= ne) {
-          count1(q[u].x); count1(q[u].y); count1(q[u].z); count1(q[u].w);
-        } else {
-          for (uint32_t t = j; t < ne && t < j + 4; ++t) count1(e.b(t));
-        }
-      }
-    }
+#pragma unroll 1
+    for (uint32_t j = lane; j < e.n; j += 32) count1(e.b(j));
   } else {
     // Whole slab.  Lane l owns the 16 consecutive elements [16l, 16l + 16) of each 512-element
     // round (four 128-bit loads; a warp instruction touches every other 16 B, its neighbour
@@ -1050,8 +1063,10 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
   const int32_t* s_key = reinterpret_cast<const int32_t*>(sc->cand_key);  // sorted, in shared memory
   uint32_t* s_h = hs.h;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  TK_TRACE(20);
   for (int i = threadIdx.x; i < NB; i += THREADS) s_h[i] = 0u;
   __syncthreads();
+  TK_TRACE(21);
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const Entries e = warp_entries(cp, sc->cmp_bottom, gw, warp);
   const uint32_t ne = e.n;
@@ -1062,29 +1077,17 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
     for (int l = LEV - 1; l >= 0; --l) b += (a >= s_key[b + (1u << l) - 1]) ? (1u << l) : 0u;
     atomicAdd(&s_h[b], 1u);
   };
-  for (uint32_t j0 = 0; j0 < ne; j0 += 512) {
-    uint4 q[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t j = j0 + u * 128 + 4 * lane;
-      q[u] = make_uint4(0u, 0u, 0u, 0u);
-      if (j + 4 <= ne) q[u] = e.b4(j);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t j = j0 + u * 128 + 4 * lane;
-      if (j + 4 <= ne) {
-        add(q[u].x); add(q[u].y); add(q[u].z); add(q[u].w);
-      } else {
-        for (uint32_t t = j; t < ne && t < j + 4; ++t) add(e.b(t));
-      }
-    }
-  }
+  // a warp holds few entries in the EF-pass regime (~15 at C2): one per lane per iteration keeps
+  // this once-per-launch code small (its instructions are fetched cold every launch)
+#pragma unroll 1
+  for (uint32_t j = lane; j < ne; j += 32) add(e.b(j));
   __syncthreads();
+  TK_TRACE(22);
   for (int b = threadIdx.x; b < NB; b += THREADS) {
     const uint32_t t = s_h[b];
     if (b > 0 && t) atomicAdd(ghist + (blockIdx.x & (HREP - 1)) * TOT_STRIDE + b, t);  // bucket 0 is never needed
   }
+  TK_TRACE(23);
   if (suf) {
     __shared__ uint32_t s_sw[WARPS];
     uint32_t v[4], sum = 0;
@@ -1122,13 +1125,19 @@ __device__ __forceinline__ void load_totals(const uint32_t* tot_p, int nk, uint3
 __device__ __forceinline__ void hist_to_counts(const uint32_t* ghist, int lev, uint32_t* s_tot) {
   __shared__ uint32_t s_w[WARPS];
   const int NB = 1 << lev;
-  uint32_t v[4], sum = 0;
+  uint32_t x[4][HREP];  // every load issued before any is used
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int b = NB - 1 - (4 * (int)threadIdx.x + q);
+#pragma unroll
+    for (int c = 0; c < HREP; ++c) x[q][c] = b >= 1 ? __ldcg(ghist + c * TOT_STRIDE + b) : 0u;
+  }
+  uint32_t v[4], sum = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
     v[q] = 0u;
-    if (b >= 1)
-      for (int c = 0; c < HREP; ++c) v[q] += __ldcg(ghist + c * TOT_STRIDE + b);
+#pragma unroll
+    for (int c = 0; c < HREP; ++c) v[q] += x[q][c];
     sum += v[q];
   }
   uint32_t total;
@@ -1179,8 +1188,8 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
                                           const Compact cp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t gw = blockIdx.x * WARPS + warp;
-  const uint64_t lo = min(sp.n, (uint64_t)gw * sp.S);
-  const uint64_t hi = min(sp.n, lo + sp.S);
+  uint64_t lo, hi;
+  warp_slab(sp, warp, lo, hi);
   if (lo >= hi) return;
   const int32_t p1 = c->prov1, p2 = c->prov2;
   const int32_t key1 = (p1 >= 0) ? (int32_t)c->key1 : (int32_t)INF_BITS;
@@ -1357,7 +1366,7 @@ struct Fused {
                              // without EF), nullptr (acc = g)
   const float* acc;          // the vector MSTopK reads: accw or g
   uint32_t units_per_warp;   // ef phase: aligned power-of-two run of 512-element units per warp
-  double* cta_sum;           // [grid] ef partials
+  double* cta_sum;           // [grid] ef partials: one aligned canonical-tree subtree per CTA
   uint32_t* cta_max;         // [grid]
   uint32_t* wcnt;            // [npass * TMAX][W] per-warp-slab trial counts
   uint32_t* totals;          // [npass][16] global trial counts
@@ -1465,6 +1474,7 @@ __device__ __forceinline__ uint32_t exact_split(const Ctrl* c, uint32_t j, uint3
 #ifndef TK_MIN_BLOCKS
 #define TK_MIN_BLOCKS 3
 #endif
+
 template <bool EF, int NP, int SEL>
 __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   static_assert(SEL == SEL_MSTOPK || SEL == SEL_EXACT || SEL == SEL_PROSE, "selector");
@@ -1477,9 +1487,19 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ uint64_t bar_t;  // thread 0: target of the next grid barrier (shared: keeps it out of registers)
   if (tid == 0) bar_t = grid_sync_base(f.bar);
-  ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)
+  if (lane == 0) g_es.run[warp] = warp_run_of(f.sp, blockIdx.x * WARPS + warp);
+  ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)  (syncs the CTA)
   int nph = 0;
+  auto gsync = [&]() __attribute__((always_inline)) {
+#ifdef TK_PHASE_TRACE
+    if (tid == 0 && nph < 32 && blockIdx.x < 2048) g_trace[1][nph][blockIdx.x] = globaltimer();
+#endif
+    grid_sync(f.bar, bar_t);
+  };
   auto stamp = [&]() {
+#ifdef TK_PHASE_TRACE
+    if (tid == 0 && nph < 32 && blockIdx.x < 2048) g_trace[0][nph][blockIdx.x] = globaltimer();
+#endif
     if (tid == 0 && nph < 12) sc.phase_ns[nph] = globaltimer();
     ++nph;
     sc.n_phase = (uint32_t)min(nph, 12);
@@ -1496,7 +1516,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   uint32_t* cta_ent = f.cta_cls + 3 * gridDim.x;
   ef_phase<EF, NP>(f.g, f.pr, f.r, f.accw, f.sp, f.units_per_warp, f.cta_sum, f.cta_max, efk, f.cp, f.flags + 2,
                    f.seq, cta_ent);
-  grid_sync(f.bar, bar_t);
+  gsync();
   stamp();
   const uint32_t of2 = __ldcg(f.flags + 2);
   stats_root<SEL>(f.cta_sum, f.cta_max, cta_ent, f.sp, &sc, f.step);
@@ -1563,7 +1583,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       }
       __syncthreads();
       run_count<3, COUNT_FIRST>(f, &sc, 0);
-      grid_sync(f.bar, bar_t);
+      gsync();
       stamp();
       load_totals(f.totals, 3, s_tot);
       if (tid == 0) {
@@ -1610,7 +1630,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
         else
           run_count<3, COUNT_FULL>(f, &sc, p);
       }
-      grid_sync(f.bar, bar_t);
+      gsync();
       stamp();
       if (mode == 0) hist_to_counts(tot_p, HIST_LEV, s_tot);
       else load_totals(tot_p, 3, s_tot);
@@ -1643,7 +1663,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       }
       __syncthreads();
       run_count<2, COUNT_FULL>(f, &sc, p);
-      grid_sync(f.bar, bar_t);
+      gsync();
       stamp();
     }
     if (tid == 0) {
@@ -1691,6 +1711,12 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
     if (fast) {
       make_candidates_par<SEL>(&sc, min(min(HIST_LEV, f.cap_levels), N));
       __syncthreads();
+#ifdef TK_ICACHE_EXPERIMENT  // trace builds: the same (idempotent) work again, now with warm caches
+      TK_TRACE(24);
+      make_candidates_par<SEL>(&sc, min(min(HIST_LEV, f.cap_levels), N));
+      __syncthreads();
+      TK_TRACE(25);
+#endif
     }
     for (; done < N; ++p) {
       int lev;
@@ -1723,7 +1749,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
         lev = min(min(2, f.cap_levels), N - done);
         if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<3, COUNT_FULL>(f, &sc, p);
       }
-      grid_sync(f.bar, bar_t);
+      gsync();
       stamp();
       if (hist) hist_to_counts(tot_p, lev, s_tot);
       else load_totals(tot_p, 16, s_tot);
@@ -1795,7 +1821,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       }
       __syncthreads();
       run_count<8, COUNT_FULL>(f, &sc, pnext);
-      grid_sync(f.bar, bar_t);
+      gsync();
       stamp();
       load_totals(f.totals + HIST_BINS * HREP * pnext, 8, s_tot);
       if (tid == 0) {
@@ -1833,8 +1859,8 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   // ---- A7 prefix: class-1 / class-2 counts of each warp slab, then of the CTAs before it ----
   const uint32_t gw = blockIdx.x * WARPS + warp;
   const uint32_t W = f.sp.W;
-  const uint64_t slo = min(f.sp.n, (uint64_t)gw * f.sp.S);
-  const uint64_t shi = min(f.sp.n, slo + f.sp.S);
+  uint64_t slo, shi;
+  warp_slab(f.sp, warp, slo, shi);
   uint32_t c1 = 0, call = 0;
   if (lane == 0) s_ne[warp] = 0u;
   if (sc.cap_ok) {
@@ -1871,7 +1897,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       f.cta_cls[gridDim.x + blockIdx.x] = t2;
       f.cta_cls[2 * gridDim.x + blockIdx.x] = tn;  // compacted entries (statistics)
     }
-    grid_sync(f.bar, bar_t);
+    gsync();
   }
   stamp();
   {
@@ -1956,6 +1982,10 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
     }
     ctrl_to_global(f.c, &sc);
   }
+#ifdef TK_PHASE_TRACE
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < 2048) g_trace[0][31][blockIdx.x] = globaltimer();  // end of this CTA
+#endif
 }
 
 // ------------------------------------------------------------------------------------------
