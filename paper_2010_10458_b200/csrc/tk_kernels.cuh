@@ -114,6 +114,8 @@ struct Ctrl {
   double cand_ratio[NPATH_CAND];    // coordinate (ratio / threshold) of path candidates
   double cand_t[NPATH_CAND];        // and their thresholds
   uint32_t cand_key[HIST_BINS];     // candidate keys (ascending for a tree / histogram pass)
+  double tree_t[HIST_BINS];         // tree candidates' thresholds, kept by make_candidates_par so the serial
+  double tree_lo, tree_w, tree_scale;  // replay recomputes none; ratio of node m = lo + w * (m * scale)
 };
 constexpr int CTRL_HEADER_WORDS = (int)(offsetof(Ctrl, ratio_log) / 4);
 constexpr int CTRL_KEEP_WORDS = (int)(offsetof(Ctrl, cand_ratio) / 4);
@@ -314,13 +316,18 @@ __device__ __forceinline__ void make_candidates_par(Ctrl* c, int lev) {
         half >>= 1;
       }
       c->cand_key[m - 1] = key_of(t);
+      c->tree_t[m - 1] = t;
     }
   } else {
     const double w = __dsub_rn(c->hi, c->lo);
+    const double scale = __longlong_as_double((long long)(1023 - lev) << 52);  // 2^-lev, exact
     for (int m = (int)threadIdx.x + 1; m <= T; m += THREADS) {
-      const double ratio = __dadd_rn(c->lo, __dmul_rn(w, (double)m * ldexp(1.0, -lev)));
-      c->cand_key[m - 1] = key_of(threshold_of(c->abar, c->U, ratio));
+      const double ratio = __dadd_rn(c->lo, __dmul_rn(w, (double)m * scale));
+      const double t = threshold_of(c->abar, c->U, ratio);
+      c->cand_key[m - 1] = key_of(t);
+      c->tree_t[m - 1] = t;
     }
+    if (threadIdx.x == 0) { c->tree_lo = c->lo; c->tree_w = w; c->tree_scale = scale; }
   }
   if (threadIdx.x == 0) {
     c->ncand = (uint32_t)T;
@@ -341,6 +348,43 @@ __device__ __forceinline__ int replay_levels(Ctrl* c, const uint32_t* totals, in
   const bool tree = ((nc + 1) & nc) == 0 && c->cand_tree;
   int m = (nc + 1) >> 1, stepm = m >> 1;  // tree walk: 1-based node index and half-width
   int l = 0;
+  if (tree) {
+    // node m of the complete subtree is exactly this level's trial (Alg. 1: its ratio is dyadic,
+    // so lo + (hi-lo)*m/2^L equals the sequential midpoints, Q5; prose: the candidate walked the
+    // same decisions): coordinate, threshold and key as make_candidates_par kept them.  The state
+    // lives in registers for the walk (this serial chain is on the kernel's critical path).
+    uint32_t it = c->it, k1 = c->k1, k2 = c->k2, key1 = c->key1, key2 = c->key2;
+    double thres1 = c->thres1, thres2 = c->thres2, lo = c->lo, hi = c->hi;
+    int32_t prov1 = c->prov1, prov2 = c->prov2;
+    const double tlo = c->tree_lo, tw = c->tree_w, tscale = c->tree_scale;
+    for (; l < max_lev && m >= 1 && m <= nc; ++l) {
+      const int s = m - 1;
+      const uint32_t nnz = totals[s], key = c->cand_key[s];
+      const double t = c->tree_t[s];
+      const double ratio = (SEL == SEL_PROSE) ? t : __dadd_rn(tlo, __dmul_rn(tw, (double)m * tscale));
+      c->ratio_log[it] = (SEL == SEL_PROSE) ? __longlong_as_double(0x7FF8000000000000ll) : ratio;  // prose: no ratio
+      c->thres_log[it] = t;
+      c->key_log[it] = key;
+      c->nnz_log[it] = nnz;
+      ++it;
+      const bool gt = (uint64_t)nnz > k;
+      if (!gt) {                           // l.11
+        hi = ratio;                        // l.12 (prose: the bracket, re-derived below)
+        if (nnz > k1) { k1 = nnz; thres1 = t; key1 = key; prov1 = pass * TMAX + s; }  // l.13-15
+        m -= stepm;
+      } else {                             // l.17
+        lo = ratio;                        // l.18
+        if (nnz < k2) { k2 = nnz; thres2 = t; key2 = key; prov2 = pass * TMAX + s; }  // l.19-21
+        m += stepm;
+      }
+      if constexpr (SEL == SEL_PROSE) prose_advance(c->pt, c->lo, c->hi, c->lo_set, c->hi_set, gt);
+      stepm >>= 1;
+    }
+    c->it = it; c->k1 = k1; c->k2 = k2; c->key1 = key1; c->key2 = key2;
+    c->thres1 = thres1; c->thres2 = thres2; c->prov1 = prov1; c->prov2 = prov2;
+    if constexpr (SEL != SEL_PROSE) { c->lo = lo; c->hi = hi; }
+    return l;
+  }
   for (; l < max_lev; ++l) {
     double ratio, t;
     if constexpr (SEL == SEL_PROSE) {
@@ -1488,6 +1532,13 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   __shared__ uint64_t bar_t;  // thread 0: target of the next grid barrier (shared: keeps it out of registers)
   if (tid == 0) bar_t = grid_sync_base(f.bar);
   if (lane == 0) g_es.run[warp] = warp_run_of(f.sp, blockIdx.x * WARPS + warp);
+#ifdef TK_PHASE_TRACE
+  if (tid == 0 && blockIdx.x < 2048) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[1][30][blockIdx.x] = smid;
+  }
+#endif
   ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)  (syncs the CTA)
   int nph = 0;
   auto gsync = [&]() __attribute__((always_inline)) {

@@ -23,6 +23,8 @@ for s in range(200):
         t0 = st[0, :G].min()
         acc.append((buf.astype(np.int64)[:, :, :G] - t0))
 a = np.stack(acc)  # [samples][2][32][G]
+smid = buf[1, 30, :G].astype(np.int64)
+np.savez(os.environ.get("TRACE_OUT", "/tmp/trace.npz"), a=a, smid=smid)
 n = len(acc)
 print(f"d={d} CTAs={G} samples={n} (us, relative to the earliest CTA start; median over samples of min/med/max over CTAs)")
 for kind, name in ((0, "stamp"), (1, "arrive")):
