@@ -294,7 +294,14 @@ tk_status plan_launches(tk_ctx* c) {
   const uint64_t L = c->L;
   const uint64_t rounds = (L + ROUND - 1) / ROUND;
   // persistent cooperative grid: every CTA resident; no more CTAs than warp rounds of work
-  c->grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sms * occ, (rounds + WARPS - 1) / WARPS));
+  // units per warp >= TK_MIN_UNITS_PER_WARP.  Measured at d = 1M / 4M (tools/c1_probe.py): 4 or 8
+  // units per warp (61 / 31 CTAs at 1M) make the ef phase 2-3x slower than they save in the
+  // barrier-bound tail, so every warp gets >= 1 unit and the grid stays as wide as the SMs allow
+#ifndef TK_MIN_UNITS_PER_WARP
+#define TK_MIN_UNITS_PER_WARP 1
+#endif
+  const uint64_t per_cta = (uint64_t)WARPS * TK_MIN_UNITS_PER_WARP;
+  c->grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sms * occ, (rounds + per_cta - 1) / per_cta));
   c->grid = std::min<uint32_t>(c->grid, 4096);  // stats_root folds <= 4096 CTA partials
   c->W = c->grid * WARPS;
   uint64_t upw = 1;  // ef phase: aligned power-of-two run of units per warp covering the vector

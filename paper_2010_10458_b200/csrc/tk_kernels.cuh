@@ -97,6 +97,7 @@ struct Ctrl {
   uint32_t ef_key;       // compaction key of the NEXT call's ef phase (0: none), set at the end of a call
   uint32_t ef_used;      // this call's selection ran on the ef-phase entries
   uint32_t prev_key2;    // MSTopK: the previous call's key2
+  uint32_t mv_est;       // decaying maximum of the recent moves of key2 (exact selector: of T), in key units
   uint64_t nnz_lb;       // trials whose count was not taken (their key lay below the ef-phase key, so
                          // only "nnz > k" is known); cleared when exact_trial_counts counts them
   // prose search (TK_SELECT_PROSE, reading Q33): the next trial threshold pt and the bracket
@@ -1100,10 +1101,11 @@ struct HistSmem {
 // suf (optional): this CTA's suffix sums S[b] = sum_{b' >= b} h[b'] of its own histogram, so that
 // after the replay each CTA can read the class counts of the CTAs before it without another
 // grid barrier (#entries of CTA c at or above candidate s = S_c[s + 1]).
-template <int LEV>
-__device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uint32_t* ghist, HistSmem& hs,
+__device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uint32_t* ghist, HistSmem& hs, int LEV,
                                            uint32_t* suf = nullptr) {
-  constexpr int NB = 1 << LEV;
+  // LEV is a runtime value: one copy of this once-per-launch code instead of ten (code size and
+  // register pressure of the whole kernel)
+  const int NB = 1 << LEV;
   const int32_t* s_key = reinterpret_cast<const int32_t*>(sc->cand_key);  // sorted, in shared memory
   uint32_t* s_h = hs.h;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1117,7 +1119,7 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
   auto add = [&](uint32_t bits) {
     const int32_t a = (int32_t)(bits & 0x7FFFFFFFu);
     uint32_t b = 0;
-#pragma unroll
+#pragma unroll 1
     for (int l = LEV - 1; l >= 0; --l) b += (a >= s_key[b + (1u << l) - 1]) ? (1u << l) : 0u;
     atomicAdd(&s_h[b], 1u);
   };
@@ -1663,7 +1665,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       if (mode == 0) {
         for (int j = tid; j < HIST_BINS - 1; j += THREADS) sc.cand_key[j] = exact_split(&sc, j + 1, HIST_BINS);
         __syncthreads();
-        hist_phase<HIST_LEV>(&sc, f.cp, tot_p, s_hist);
+        hist_phase(&sc, f.cp, tot_p, s_hist, HIST_LEV);
       } else {
         if (tid == 0) {
           if (mode == 1) {
@@ -1735,8 +1737,9 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       sc.prev_T = T;
       // next call's ef-phase compaction key: below T by half its last move if T rose (error
       // feedback grows the residual), else twice it, plus a margin
-      const uint32_t mv = min(sc.prev_dT, 1u << 22);
-      const uint32_t delta = min(1u << 22, ((P > 0u && T > P) ? mv / 2u : 2u * mv) + (1u << 10));
+      const uint32_t est = max(min(sc.prev_dT, 1u << 22), sc.mv_est / 2u);  // as for MSTopK's key2 below
+      sc.mv_est = est;
+      const uint32_t delta = min(1u << 22, 2u * est + (1u << 14));
       sc.ef_key = T > delta ? T - delta : 0u;
     }
     __syncthreads();
@@ -1784,18 +1787,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       } else if (sc.cap_ok) {
         hist = true;
         lev = min(min(HIST_LEV, f.cap_levels), N - done);
-        switch (lev) {
-          case 1: hist_phase<1>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 2: hist_phase<2>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 3: hist_phase<3>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 4: hist_phase<4>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 5: hist_phase<5>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 6: hist_phase<6>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 7: hist_phase<7>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 8: hist_phase<8>(&sc, f.cp, tot_p, s_hist, suf); break;
-          case 9: hist_phase<9>(&sc, f.cp, tot_p, s_hist, suf); break;
-          default: hist_phase<10>(&sc, f.cp, tot_p, s_hist, suf); break;
-        }
+        hist_phase(&sc, f.cp, tot_p, s_hist, lev, suf);
       } else {
         lev = min(min(2, f.cap_levels), N - done);
         if (lev == 1) run_count<1, COUNT_FULL>(f, &sc, p); else run_count<3, COUNT_FULL>(f, &sc, p);
@@ -1893,10 +1885,13 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
     if (sc.prov2 >= 0) {
       const uint32_t P = sc.prev_key2;
       const uint32_t dk = (P > 0u) ? (K > P ? K - P : P - K) : (1u << 21);
-      // a rising key2 (error feedback grows the residual) is expected to keep rising: half the
-      // last move below it; a falling one: twice the last move
-      const uint32_t mv = min(dk, 1u << 22);
-      const uint32_t margin = min(1u << 22, ((P > 0u && K > P) ? mv / 2u : 2u * mv) + (1u << 12));
+      // the margin below key2 covers twice the largest recent move (decaying by half per call):
+      // a prediction that fails costs a whole-vector restart (~20 us at C2), a generous margin
+      // only a few thousand more entries (measured: i.i.d. inputs without error feedback move key2
+      // both ways by ~20-60K ulps per call; with EF it mostly rises)
+      const uint32_t est = max(min(dk, 1u << 22), sc.mv_est / 2u);
+      sc.mv_est = est;
+      const uint32_t margin = min(1u << 22, 2u * est + (1u << 14));
       sc.ef_key = K > margin ? K - margin : 0u;
       sc.prev_key2 = K;
     } else {

@@ -99,6 +99,12 @@ __global__ void k(uint32_t* bar, int iters, uint32_t base) {
   }
 }
 __global__ void empty_k() {}
+__global__ void empty_smem(uint32_t* p) {
+  __shared__ uint32_t big[9000];
+  big[threadIdx.x] = threadIdx.x;
+  __syncthreads();
+  if (big[(threadIdx.x + 1) % blockDim.x] == 12345678u) p[0] = 1;
+}
 
 int main() {
   int sms;
@@ -134,6 +140,27 @@ int main() {
       }
       printf("grid %4d V%d: %.3f us per barrier (%s)\n", sms * occ, mode, best * 1e3 / iters,
              cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  // launch overhead of an empty kernel vs grid shape (CTA count, threads, static smem)
+  {
+    struct Cfg { int ctas, threads; bool smem; };
+    const Cfg cfgs[] = {{sms, 256, false}, {sms, 768, false}, {2 * sms, 256, false}, {3 * sms, 256, false},
+                        {3 * sms, 256, true}, {sms, 768, true}, {sms, 1024, false}};
+    for (const Cfg& c : cfgs) {
+      const int n = 200;
+      for (int w = 0; w < 2; ++w) {
+        cudaEventRecord(a);
+        for (int i = 0; i < n; ++i) {
+          if (c.smem) empty_smem<<<c.ctas, c.threads>>>(bar);
+          else empty_k<<<c.ctas, c.threads>>>();
+        }
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+      }
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      printf("empty launch %4d x %4d%s: %.2f us each\n", c.ctas, c.threads, c.smem ? " (36 KB smem)" : "", ms * 1e3 / n);
     }
   }
   // launch overhead: back-to-back empty cooperative launches of the full grid, and a plain launch

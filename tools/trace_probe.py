@@ -5,7 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2010_10458_b200 as tk
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 25_600_000
-ctx = tk.Context(d, rho=0.001, n_iters=10, seed=1)
+ef = os.environ.get("EF", "1") == "1"
+ctx = tk.Context(d, rho=0.001, n_iters=10, seed=1, error_feedback=ef)
 gen = torch.Generator(device="cuda"); gen.manual_seed(5)
 gs = [torch.randn(d, generator=gen, device="cuda") for _ in range(8)]
 r = torch.zeros(d, device="cuda"); out = torch.empty(d, device="cuda")
@@ -14,7 +15,10 @@ buf = np.zeros((2, 32, 2048), np.uint64)
 G = None
 acc = []
 for s in range(200):
-    ctx.step(gs[s % 8], r, out)
+    if ef:
+        ctx.step(gs[s % 8], r, out)
+    else:
+        ctx.compress(gs[s % 8], None)
     if s >= 40 and s % 10 == 0:
         torch.cuda.synchronize()
         assert lib.tk_debug_trace(ctypes.c_void_p(buf.ctypes.data)) == 0
@@ -26,7 +30,7 @@ a = np.stack(acc)  # [samples][2][32][G]
 smid = buf[1, 30, :G].astype(np.int64)
 np.savez(os.environ.get("TRACE_OUT", "/tmp/trace.npz"), a=a, smid=smid)
 n = len(acc)
-print(f"d={d} CTAs={G} samples={n} (us, relative to the earliest CTA start; median over samples of min/med/max over CTAs)")
+print(f"EF={ef} d={d} CTAs={G} samples={n} (us, relative to the earliest CTA start; median over samples of min/med/max over CTAs)")
 for kind, name in ((0, "stamp"), (1, "arrive")):
     for slot in range(32):
         v = a[:, kind, slot, :]
