@@ -59,6 +59,8 @@ def parse():
                     help="value format on the wire: fp32 or binary16 (SURVEY F3, Fig. 7's FP16)")
     ap.add_argument("--sgd", type=float, default=0.0,
                     help="lr > 0: time tk_step_sgd (Eq. 1's update fused into the decompression, SURVEY F4)")
+    ap.add_argument("--no-symmetric", action="store_true",
+                    help="HiTopKComm: plain gradient / output tensors (copy-in, NCCL row all-gather)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no soak, no e2e, no cpu baseline")
@@ -314,6 +316,53 @@ def stage_bytes(name, L, d, k, P, ef, chunks):
     return None
 
 
+NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md); 900 nominal
+
+
+def nvlink_report(a, stages, P, n, L, k, t_step_ms, cw):
+    """Bytes each GPU must move over NVLink per step for every exchange of the path, and the
+    achieved rate over the stage that carries it, against the measured 770 GB/s per direction
+    (Eq. 3 for the flat all-gather, Eqs. 7-10 for HiTopKComm's steps)."""
+    if P == 1:
+        return None
+    m = P // n
+
+    def st(name):
+        v = stages.get(name)
+        return v["ms_per_launch"] * v["launches_per_step"] if v else None
+
+    def entry(nbytes, ms, carried_by):
+        out = {"bytes_per_gpu": nbytes, "stage": carried_by}
+        if ms:
+            out.update({"ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9, "frac": nbytes / (ms * 1e-3) / 1e9 / NVLINK_GBS})
+        return out
+    rep = {"peak_GBps": NVLINK_GBS, "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)"}
+    if n == 1:
+        ag = 4 * (P - 1) * cw  # received: every other rank's packed chunk (8k B with fp32 values)
+        if a.ag_mode == "push":
+            # fused: the packets are pushed by k_compress and consumed by k_decompress; the exchange
+            # has no stage of its own, so the whole step bounds it
+            rep["allgather"] = entry(ag, t_step_ms, "fused into k_compress + k_decompress (step time as the bound)")
+        else:
+            rep["allgather"] = entry(ag, st("allgather"), "ncclAllGather")
+        rep["allgather"]["time_at_peak_us"] = ag / NVLINK_GBS / 1e3
+        return rep
+    rs = 4 * (n - 1) * L  # H1: the peer segments this GPU reads (ordered RS fused into the EF pass)
+    rep["h1_reduce_scatter"] = entry(rs, st("k_compress") if a.rs_mode == "ordered" else st("reduce_scatter"),
+                                     "k_compress (peer loads)" if a.rs_mode == "ordered" else "ncclReduceScatter")
+    rep["h3_column_allgather"] = entry(4 * (m - 1) * cw, st("allgather"), "ncclAllGather (column)")
+    if a.step4 == "dense":
+        s4 = 4 * (n - 1) * L
+        t4 = (st("k_decompress") or 0) + (st("step4_allgather") or 0)
+        rep["h5_row_allgather"] = entry(s4, t4, "k_decompress replica stores + row barrier" if not a.no_symmetric
+                                        else "k_decompress + ncclAllGather (row)")
+    else:
+        rep["h5_row_allgather"] = entry(4 * (n - 1) * m * cw, st("step4_allgather"), "ncclAllGather (row, pairs)")
+    for key in ("h1_reduce_scatter", "h3_column_allgather", "h5_row_allgather"):
+        rep[key]["time_at_peak_us"] = rep[key]["bytes_per_gpu"] / NVLINK_GBS / 1e3
+    return rep
+
+
 def log(*x):
     print(f"[bench {time.strftime('%H:%M:%S')}]", *x, file=sys.stderr, flush=True)
 
@@ -351,16 +400,24 @@ def main():
     # the device before any timing (pool capped at ~16 GB per rank; reused cyclically beyond that)
     need = a.warmup + 2 * a.steps
     nbuf = max(2, min(need, int(16e9 // (4 * a.d))))
+    # HiTopKComm with the ordered reduce-scatter: the gradients live in symmetric (IPC-mapped)
+    # buffers, as a training loop would produce them (no per-step copy-in), and so does out (the
+    # dense step 4 is then fused into the decompression)
+    sym = n > 1 and a.rs_mode == "ordered" and not a.no_symmetric
+    if sym:
+        nbuf = min(nbuf, 8)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(201010458 + 1000 * rank)
     with torch.cuda.stream(stream):
-        if a.dist == "G":
-            gs = [torch.randn(a.d, generator=gen, device="cuda", dtype=torch.float32) for _ in range(nbuf)]
-        else:
-            gs = [torch.from_numpy(gradgen.gradient(a.d, a.dist, cfg=2, rank=rank, step=s)).cuda() for s in range(nbuf)]
+        gs = [ctx.alloc_symmetric(a.d) if sym else torch.empty(a.d, device="cuda") for _ in range(nbuf)]
+        for s_, gt in enumerate(gs):
+            if a.dist == "G":
+                gt.normal_(generator=gen)
+            else:
+                gt.copy_(torch.from_numpy(gradgen.gradient(a.d, a.dist, cfg=2, rank=rank, step=s_)))
         r = torch.zeros(L, dtype=torch.float32, device="cuda")
         r_soak = torch.zeros(L, dtype=torch.float32, device="cuda")
-        out = torch.empty(a.d, dtype=torch.float32, device="cuda")
+        out = ctx.alloc_symmetric(a.d) if sym else torch.empty(a.d, dtype=torch.float32, device="cuda")
         w = torch.randn(a.d, generator=gen, device="cuda", dtype=torch.float32) if a.sgd else None
     stream.synchronize()
     cursor = [0]
@@ -451,6 +508,31 @@ def main():
                 "note": "achieved = algorithmic bytes per launch (the floor: 12 B/elem (EF: read g, r; write acc) "
                         "+ 12 B/pair) / mean CUDA-event duration of that launch inside the profiled steps"}
 
+    nvlink = nvlink_report(a, stages, P, n, L, k, t_step, ctx.chunk_words)
+    # comparator: the dense all-reduce of the whole fp32 gradient the sparse path replaces (the paper's
+    # TreeAR / dense baseline): ncclAllReduce of 4d bytes, max over ranks
+    allreduce = None
+    if P > 1 and not a.ncu:
+        import torch.distributed as dist
+        buf = gs[0].clone()
+        for _ in range(3):
+            dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        barrier(ws)
+        ka = max(5, min(a.steps, 20))
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        for _ in range(ka):
+            dist.all_reduce(buf)
+        eb.record()
+        torch.cuda.synchronize()
+        t_ar = max_over_ranks(ea.elapsed_time(eb) / ka, ws)
+        allreduce = {"ms": t_ar, "elements_per_s": P * a.d / (t_ar * 1e-3),
+                     "bus_GBps": 2 * (P - 1) / P * 4 * a.d / (t_ar * 1e-3) / 1e9,
+                     "sparse_step_speedup": t_ar / t_step,
+                     "note": "torch.distributed.all_reduce (NCCL) of the dense fp32 gradient, max over ranks"}
+        del buf
+
     # end-to-end through the public host-buffer API: pinned H2D of g + D2H of the gathered pairs
     e2e = None
     if not a.no_e2e and not a.ncu:
@@ -505,7 +587,8 @@ def main():
                            "l2": "inputs larger than L2: each step reads a fresh g (4d B) and touches r and out: "
                                  f"{12 * a.d / 1e6:.0f} MB per rank per step vs 126 MB L2; no explicit flush"},
                 "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
-                "e2e": e2e, "stages": stages, "recall_vs_exact": recall}
+                "e2e": e2e, "stages": stages, "recall_vs_exact": recall, "nvlink": nvlink,
+                "dense_allreduce_comparator": allreduce}
         emit(line)
     ctx.close()
     if ws > 1:

@@ -238,9 +238,10 @@ tk_status tk_step_sgd(tk_ctx* ctx, const float* g, float* r, float* w, float lr,
  * dense aggregate back to out_host.  Synchronises the context stream. */
 tk_status tk_step_host(tk_ctx* ctx, const float* g_host, uint32_t* gathered_host, float* out_host);
 
-/* HiTopKComm with TK_RS_ORDERED: the context's peer-visible gradient buffer ([d] fp32, device).
- * A caller that writes its gradient here and passes this pointer as g to tk_step avoids the
- * copy-in (tk_step copies any other g into it first).  NULL for flat mode. */
+/* HiTopKComm with TK_RS_ORDERED: the context's own symmetric gradient buffer ([d] fp32, device).
+ * A caller that writes its gradient here (or into a tk_alloc_symmetric buffer) and passes that
+ * pointer as g to tk_step avoids the copy-in (tk_step copies any other g into this buffer first).
+ * Same usage contract as the symmetric buffers below.  NULL for flat mode. */
 tk_status tk_input_buffer(tk_ctx* ctx, float** g);
 
 /* --- loopback (cfg.loopback = 1): single-GPU emulation of the fused all-gather ----
@@ -259,6 +260,26 @@ tk_status tk_loopback_push(tk_ctx* ctx, const float* g, float* r, uint32_t* chun
                            uint32_t nslots, uint32_t tag);
 tk_status tk_loopback_decompress(tk_ctx* ctx, const void* packets, uint32_t nchunks, uint32_t tag, float* out,
                                  uint32_t* plain_out);
+
+/* Symmetric buffers (HiTopKComm with TK_RS_ORDERED; collective over the n GPUs of a virtual node):
+ * every row peer allocates one of the same size in the same order; each GPU's copy is mapped into
+ * its peers (CUDA IPC over NVLink).  A gradient g passed to tk_step from inside a symmetric buffer
+ * is read in place by the ordered reduce-scatter (no copy into the input buffer); an out inside one
+ * (all d floats) makes the dense step 4 part of the decompression: each GPU writes its aggregated
+ * segment straight into every row peer's out (NVLink stores), and a 4-byte row all-reduce
+ * completes the exchange instead of an ncclAllGather.  Usage contract: every peer passes g (and
+ * out) at the same offset of corresponding buffers; a buffer passed as g to step s must not be
+ * rewritten by anyone before step s's call has completed on the context stream (the step's row
+ * all-gather / barrier orders every peer's reads before that).  Freeing synchronises the stream;
+ * free only when no peer can still read the buffer. */
+tk_status tk_alloc_symmetric(tk_ctx* ctx, size_t bytes, void** p);
+tk_status tk_free_symmetric(tk_ctx* ctx, void* p);
+
+/* Rank-ordered decompression (as tk_decompress) written to nout outputs at once: outs[0] and the
+ * replicas outs[1..nout) (e.g. the node peers' copies of a segment; nout in [1, 9]).  tk_step
+ * uses it for HiTopKComm's fused dense step 4. */
+tk_status tk_decompress_replicated(tk_ctx* ctx, const uint32_t* gathered, uint32_t nchunks, float* const* outs,
+                                   uint32_t nout);
 
 /* Copy the control block of the last compression to *st (synchronises the stream). */
 tk_status tk_get_stats(tk_ctx* ctx, tk_stats* st);

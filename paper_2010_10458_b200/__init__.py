@@ -66,7 +66,7 @@ EXPORTS = ["tk_k", "tk_get_unique_id", "tk_init", "tk_compress", "tk_sparse_allg
            "tk_step", "tk_step_host", "tk_get_stats", "tk_set_step", "tk_query", "tk_launch_count",
            "tk_destroy", "tk_status_string", "tk_last_error", "tk_profile_begin", "tk_profile_end",
            "tk_stage_name", "tk_input_buffer", "tk_step_sgd", "tk_compress_segment", "tk_loopback_push",
-           "tk_loopback_decompress"]
+           "tk_loopback_decompress", "tk_alloc_symmetric", "tk_free_symmetric", "tk_decompress_replicated"]
 NSTAGES = 16
 
 
@@ -101,6 +101,9 @@ def _load():
         "tk_compress_segment": (I32, [P, ctypes.POINTER(P), U32, P, P, P]),
         "tk_loopback_push": (I32, [P, P, P, P, ctypes.POINTER(P), U32, U32]),
         "tk_loopback_decompress": (I32, [P, P, U32, U32, P, P]),
+        "tk_alloc_symmetric": (I32, [P, ctypes.c_size_t, ctypes.POINTER(P)]),
+        "tk_free_symmetric": (I32, [P, P]),
+        "tk_decompress_replicated": (I32, [P, P, U32, ctypes.POINTER(P), U32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -390,6 +393,31 @@ class Context:
                      compacted=bool(s.compacted), n_compacted=int(s.n_compacted),
                      phase_us=[(s.phase_ns[i + 1] - s.phase_ns[i]) / 1e3 for i in range(max(0, s.n_phases - 1))],
                      ef_compacted=bool(s.ef_compacted), nnz_not_counted=int(s.nnz_not_counted))
+
+    def decompress_replicated(self, gathered, outs, nchunks=None):
+        """tk_decompress_replicated: the rank-ordered decompression written to every tensor in outs
+        (each out_len floats) - HiTopKComm's fused dense step 4 writes a segment to the node peers."""
+        outs = list(outs)
+        nch = self.chunks if nchunks is None else int(nchunks)
+        arr = (ctypes.c_void_p * len(outs))(*[self._p(t, f"outs[{i}]", torch.float32, self.out_len).value
+                                              for i, t in enumerate(outs)])
+        self._check(_lib.tk_decompress_replicated(self._ctx, self._p(gathered, "gathered", torch.int32,
+                                                                     nch * self.chunk_words), nch, arr, len(outs)))
+        return outs
+
+    def alloc_symmetric(self, numel: int):
+        """tk_alloc_symmetric (collective over the GPUs of a virtual node): a float32 tensor of numel
+        elements whose peers' copies libtk maps; pass it as g (or out) to step() to skip the copy-in
+        (or to fuse the dense step 4).  Lives until free_symmetric / close."""
+        p = ctypes.c_void_p()
+        self._check(_lib.tk_alloc_symmetric(self._ctx, 4 * int(numel), ctypes.byref(p)))
+        t = _DeviceView(p.value, int(numel), self.device).tensor()
+        self._syms = getattr(self, "_syms", []) + [t]
+        return t
+
+    def free_symmetric(self, t):
+        self._check(_lib.tk_free_symmetric(self._ctx, ctypes.c_void_p(t.data_ptr())))
+        self._syms = [x for x in getattr(self, "_syms", []) if x.data_ptr() != t.data_ptr()]
 
     def input_buffer(self):
         """HiTopKComm ordered mode: a torch view of libtk's peer-visible gradient buffer (write the

@@ -68,6 +68,12 @@ struct tk_ctx {
   ncclComm_t world = nullptr, row = nullptr, col = nullptr;
   float* sym_g = nullptr;             // HiTopKComm ordered RS: this GPU's peer-visible gradient [d]
   float* peer_g[8] = {nullptr};       // row peers' sym_g (IPC-opened; [row_pos] = sym_g)
+  struct Sym {                        // symmetric buffers (tk_alloc_symmetric): every row peer holds one
+    char* base;                       // of the same size, allocated in the same collective order
+    size_t bytes;
+    char* peer[8];                    // [q] = row peer q's copy, IPC-opened ([row_pos] = base)
+  };
+  std::vector<Sym> syms;
   int32_t* sync_buf = nullptr;        // 4-byte buffer of the row barrier all-reduce
   ulonglong2* pg = nullptr;           // TK_AG_PUSH: [2][P][k] tagged packets (double-buffered)
   ulonglong2* peer_pg[8] = {nullptr}; // every rank's pg (IPC-opened; [rank] = pg)
@@ -229,7 +235,11 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
 // (fused all-gather) from tagged packets, optionally re-emitting the pairs in the plain layout.
 template <class Src>
 tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t kk, uint64_t len, float* out,
-                          uint32_t* plain_out = nullptr, float* w = nullptr, float lr = 0.0f) {
+                          uint32_t* plain_out = nullptr, float* w = nullptr, float lr = 0.0f,
+                          const OutReplicas* reps = nullptr) {
+  OutReplicas rp;
+  memset(&rp, 0, sizeof(rp));
+  if (reps) rp = *reps;
   const uint32_t nt = (uint32_t)((len + TILE - 1) / TILE);
   const uint32_t max_cta = c->sms * c->occ_dec;
   const uint32_t per = (nt + max_cta - 1) / max_cta;
@@ -242,7 +252,7 @@ tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t 
   }
   k_decompress<Src><<<grid, THREADS, sizeof(uint32_t) * nchunks, c->stream>>>(src, nchunks, kk, len, nt, per, out,
                                                                                plain_out, w, lr, c->cw,
-                                                                               c->cfg.wire == TK_WIRE_F16 ? 1u : 0u);
+                                                                               c->cfg.wire == TK_WIRE_F16 ? 1u : 0u, rp);
   TK_TRY(check_launch(c, "k_decompress"));
   mark(c, TK_STAGE_DECOMPRESS);
   return TK_OK;
@@ -250,10 +260,10 @@ tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t 
 
 // decompression of packed chunks in the context's wire format
 tk_status decompress_plain(tk_ctx* c, const uint32_t* base, uint32_t nchunks, uint64_t len, float* out,
-                           float* w = nullptr, float lr = 0.0f) {
+                           float* w = nullptr, float lr = 0.0f, const OutReplicas* reps = nullptr) {
   if (c->cfg.wire == TK_WIRE_F16)
-    return decompress_impl(c, PlainChunks16{base, c->k, c->cw}, nchunks, c->k, len, out, nullptr, w, lr);
-  return decompress_impl(c, PlainChunks{base, c->k}, nchunks, c->k, len, out, nullptr, w, lr);
+    return decompress_impl(c, PlainChunks16{base, c->k, c->cw}, nchunks, c->k, len, out, nullptr, w, lr, reps);
+  return decompress_impl(c, PlainChunks{base, c->k}, nchunks, c->k, len, out, nullptr, w, lr, reps);
 }
 
 // where the selection writes its values inside a packed chunk
@@ -363,6 +373,12 @@ tk_status open_row_peers(tk_ctx* c) {
   void* peers[8] = {nullptr};
   TK_TRY(exchange_ipc(c, c->row, c->n, c->row_pos, c->sym_g, peers));
   for (uint32_t q = 0; q < c->n; ++q) c->peer_g[q] = static_cast<float*>(peers[q]);
+  tk_ctx::Sym y;
+  memset(&y, 0, sizeof(y));
+  y.base = reinterpret_cast<char*>(c->sym_g);
+  y.bytes = sizeof(float) * c->d;
+  for (uint32_t q = 0; q < c->n; ++q) y.peer[q] = reinterpret_cast<char*>(peers[q]);
+  c->syms.push_back(y);
   return TK_OK;
 }
 
@@ -391,16 +407,30 @@ void free_all(tk_ctx* c) {
     delete[] c->prof_ev;
     delete[] c->prof_kind;
   }
-  for (uint32_t q = 0; q < 8; ++q)
-    if (c->peer_g[q] && c->peer_g[q] != c->sym_g) cudaIpcCloseMemHandle(c->peer_g[q]);
+  for (auto& y : c->syms) {
+    for (uint32_t q = 0; q < 8; ++q)
+      if (y.peer[q] && y.peer[q] != y.base) cudaIpcCloseMemHandle(y.peer[q]);
+    cudaFree(y.base);
+  }
+  c->syms.clear();
   for (uint32_t q = 0; q < 8; ++q)
     if (c->peer_pg[q] && c->peer_pg[q] != c->pg) cudaIpcCloseMemHandle(c->peer_pg[q]);
   if (c->pg) cudaFree(c->pg);
-  if (c->sym_g) cudaFree(c->sym_g);
   if (c->sync_buf) cudaFree(c->sync_buf);
   if (c->row) ncclCommDestroy(c->row);
   if (c->col) ncclCommDestroy(c->col);
   if (c->world) ncclCommDestroy(c->world);
+}
+
+// the symmetric buffer holding [p, p + bytes), and p's offset in it (nullptr: none)
+const tk_ctx::Sym* find_sym(const tk_ctx* c, const void* p, size_t bytes, size_t* off) {
+  const char* q = static_cast<const char*>(p);
+  for (const auto& y : c->syms)
+    if (q >= y.base && q + bytes <= y.base + y.bytes) {
+      *off = (size_t)(q - y.base);
+      return &y;
+    }
+  return nullptr;
 }
 
 }  // namespace
@@ -689,13 +719,21 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
       // peer-visible, then a row barrier (stream-ordered all-reduce of 4 bytes) so every peer's
       // copy is complete before anyone reads it.  The previous step's row all-gather (step 4)
       // already ordered every peer's last read of these buffers before this copy.
-      if (g != c->sym_g)
+      // a g inside a symmetric buffer (tk_alloc_symmetric, tk_input_buffer) is read in place by
+      // the peers; any other g is first copied into this GPU's input buffer
+      size_t goff = 0;
+      const tk_ctx::Sym* gs = find_sym(c, g, sizeof(float) * c->d, &goff);
+      if (!gs) {
         TK_CUDA(c, cudaMemcpyAsync(c->sym_g, g, sizeof(float) * c->d, cudaMemcpyDeviceToDevice, c->stream));
+        gs = find_sym(c, c->sym_g, sizeof(float) * c->d, &goff);
+        if (!gs) return fail(c, TK_ERR_STATE, "input buffer not registered");
+      }
       TK_NCCL(c, ncclAllReduce(c->sync_buf, c->sync_buf, 1, ncclInt32, ncclSum, c->row, c->stream));
       mark(c, TK_STAGE_REDUCE_SCATTER);
       Peers pr;
       memset(&pr, 0, sizeof(pr));
-      for (uint32_t q = 0; q < c->n; ++q) pr.p[q] = c->peer_g[q] + (size_t)c->row_pos * c->L;
+      for (uint32_t q = 0; q < c->n; ++q)
+        pr.p[q] = reinterpret_cast<const float*>(gs->peer[q] + goff) + (size_t)c->row_pos * c->L;
       // Step 2 (fused with step 1): MSTopK on the segment with k~ (Eq. 5), EF on the segment residual.
       TK_TRY(compress_impl(c, nullptr, ef ? r : nullptr, mine, co.val, &pr, (int)c->n, nullptr, co.val16));
     } else {
@@ -714,9 +752,26 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
     float* my_seg = out ? out + (size_t)c->row_pos * c->L : nullptr;
     if (c->cfg.step4 == TK_STEP4_DENSE) {
       // ... accumulated in group order into this GPU's segment, then step 4: dense intra-node
-      // all-gather of the segments (Alg. 2 l.21-23), in place.
-      TK_TRY(decompress_plain(c, gat, c->m, c->L, my_seg));
-      TK_NCCL(c, ncclAllGather(my_seg, out, c->L, ncclFloat32, c->row, c->stream));
+      // all-gather of the segments (Alg. 2 l.21-23).  When out is a symmetric buffer the
+      // decompression writes the segment straight into every row peer's out as well (NVLink
+      // stores, fused with step 3's accumulation), and a row barrier completes the exchange;
+      // otherwise an in-place ncclAllGather follows.
+      size_t ooff = 0;
+      const tk_ctx::Sym* os = c->cfg.loopback ? nullptr : find_sym(c, out, sizeof(float) * c->d, &ooff);
+      if (os && c->n <= 8) {
+        OutReplicas rp;
+        memset(&rp, 0, sizeof(rp));
+        for (uint32_t q = 0; q < c->n; ++q)
+          if (q != c->row_pos)
+            rp.p[rp.n++] = reinterpret_cast<float*>(os->peer[q] + ooff) + (size_t)c->row_pos * c->L;
+        TK_TRY(decompress_plain(c, gat, c->m, c->L, my_seg, nullptr, 0.0f, &rp));
+        // every peer's segment stores into this GPU's out are complete once every peer's
+        // decompression has finished: a stream-ordered 4-byte row all-reduce
+        TK_NCCL(c, ncclAllReduce(c->sync_buf, c->sync_buf, 1, ncclInt32, ncclSum, c->row, c->stream));
+      } else {
+        TK_TRY(decompress_plain(c, gat, c->m, c->L, my_seg));
+        TK_NCCL(c, ncclAllGather(my_seg, out, c->L, ncclFloat32, c->row, c->stream));
+      }
       mark(c, TK_STAGE_STEP4_ALLGATHER);
       if (w) {
         k_sgd_update<<<c->sms * 4, THREADS, 0, c->stream>>>(w, out, c->d, lr);
@@ -769,6 +824,57 @@ tk_status tk_step_host(tk_ctx* c, const float* g_host, uint32_t* gathered_host, 
     TK_CUDA(c, cudaMemcpyAsync(out_host, c->h_out, sizeof(float) * c->d, cudaMemcpyDeviceToHost, c->stream));
   TK_CUDA(c, cudaStreamSynchronize(c->stream));
   return TK_OK;
+}
+
+tk_status tk_alloc_symmetric(tk_ctx* c, size_t bytes, void** p) {
+  if (!c || !p || bytes == 0) return TK_ERR_INVALID_ARG;
+  *p = nullptr;
+  if (c->n == 1 || c->cfg.rs_mode != TK_RS_ORDERED || !c->row)
+    return fail(c, TK_ERR_STATE, "symmetric buffers belong to HiTopKComm with the ordered reduce-scatter");
+  char* base = nullptr;
+  TK_TRY(dev_alloc(c, &base, bytes));
+  void* peers[8] = {nullptr};
+  tk_status s = exchange_ipc(c, c->row, c->n, c->row_pos, base, peers);
+  if (s != TK_OK) {
+    cudaFree(base);
+    return s;
+  }
+  tk_ctx::Sym y;
+  memset(&y, 0, sizeof(y));
+  y.base = base;
+  y.bytes = bytes;
+  for (uint32_t q = 0; q < c->n; ++q) y.peer[q] = static_cast<char*>(peers[q]);
+  c->syms.push_back(y);
+  *p = base;
+  return TK_OK;
+}
+
+tk_status tk_free_symmetric(tk_ctx* c, void* p) {
+  if (!c || !p) return TK_ERR_INVALID_ARG;
+  for (size_t i = 1; i < c->syms.size(); ++i)  // [0] is the context's own input buffer
+    if (c->syms[i].base == p) {
+      TK_CUDA(c, cudaStreamSynchronize(c->stream));
+      for (uint32_t q = 0; q < 8; ++q)
+        if (c->syms[i].peer[q] && c->syms[i].peer[q] != c->syms[i].base) cudaIpcCloseMemHandle(c->syms[i].peer[q]);
+      cudaFree(c->syms[i].base);
+      c->syms.erase(c->syms.begin() + (long)i);
+      return TK_OK;
+    }
+  return fail(c, TK_ERR_INVALID_ARG, "not a symmetric buffer of this context");
+}
+
+tk_status tk_decompress_replicated(tk_ctx* c, const uint32_t* gathered, uint32_t nchunks, float* const* outs,
+                                   uint32_t nout) {
+  if (!c) return TK_ERR_INVALID_ARG;
+  if (!gathered || !outs || nout < 1 || nout > 9) return fail(c, TK_ERR_INVALID_ARG, "gathered/outs, nout in [1, 9]");
+  if (nchunks < 1 || nchunks > 4096) return fail(c, TK_ERR_INVALID_ARG, "nchunks must lie in [1, 4096]");
+  OutReplicas rp;
+  memset(&rp, 0, sizeof(rp));
+  for (uint32_t q = 0; q < nout; ++q)
+    if (!outs[q] || !aligned16(outs[q])) return fail(c, TK_ERR_INVALID_ARG, "output %u null or misaligned", q);
+  for (uint32_t q = 1; q < nout; ++q) rp.p[rp.n++] = outs[q];
+  const uint64_t len = (c->n == 1) ? c->d : c->L;
+  return decompress_plain(c, gathered, nchunks, len, outs[0], nullptr, 0.0f, &rp);
 }
 
 tk_status tk_input_buffer(tk_ctx* c, float** g) {

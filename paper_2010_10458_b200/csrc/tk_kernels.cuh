@@ -2066,6 +2066,14 @@ __device__ uint32_t warp_lower_bound(const Src& src, uint32_t p, uint32_t n, uin
   return m ? lo + (uint32_t)(__ffs(m) - 1) : hi;
 }
 
+// Replicas of the decompressed output: every tile is also written to p[0..n) (e.g. the row peers'
+// copies of this segment over NVLink: HiTopKComm's dense step 4 fused into step 3's accumulation,
+// Alg. 2 l.15-23 - each GPU writes its aggregated segment straight into every node peer's output)
+struct OutReplicas {
+  float* p[8];
+  uint32_t n;
+};
+
 // plain_out (optional): the consumed pairs re-emitted in the plain [nchunks][idx k | val k]
 // layout (each pair lies in exactly one tile, so each is written exactly once)
 // w (optional): the SGD update of Eq. 1 fused into the tile write-back,
@@ -2075,7 +2083,8 @@ template <class Src>
 __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t nchunks, uint64_t k, uint64_t n,
                                                         uint32_t ntiles, uint32_t tiles_per_cta,
                                                         float* __restrict__ out, uint32_t* __restrict__ plain_out,
-                                                        float* __restrict__ w, float lr, uint64_t cw, uint32_t w16) {
+                                                        float* __restrict__ w, float lr, uint64_t cw, uint32_t w16,
+                                                        const OutReplicas rep) {
   __shared__ __align__(16) float s_tile[TILE];
   extern __shared__ uint32_t s_cur[];  // [nchunks] per-rank cursors
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2150,6 +2159,13 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
         float4* o4 = reinterpret_cast<float4*>(out + tlo);
         for (int q = threadIdx.x; q < TILE / 4; q += THREADS) __stcs(o4 + q, s4[q]);
       }
+#pragma unroll
+      for (uint32_t r = 0; r < 8; ++r) {  // replicas (peer memory): 128-bit coalesced stores
+        if (r < rep.n) {                   // (constant indices: rep stays in parameter space)
+          float4* o4 = reinterpret_cast<float4*>(rep.p[r] + tlo);
+          for (int q = threadIdx.x; q < TILE / 4; q += THREADS) __stcs(o4 + q, s4[q]);
+        }
+      }
       if (w) {
         float4* w4 = reinterpret_cast<float4*>(w + tlo);
         for (int q = threadIdx.x; q < TILE / 4; q += THREADS) {
@@ -2166,6 +2182,9 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
       for (int q = threadIdx.x; q < TILE; q += THREADS)
         if ((uint64_t)tlo + q < n) {
           if (out) out[tlo + q] = s_tile[q];
+#pragma unroll
+          for (uint32_t r = 0; r < 8; ++r)
+            if (r < rep.n) rep.p[r][tlo + q] = s_tile[q];
           if (w) w[tlo + q] = __fsub_rn(w[tlo + q], __fmul_rn(lr, s_tile[q]));
         }
     }

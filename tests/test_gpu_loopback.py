@@ -254,3 +254,37 @@ def test_push_allgather_timeout_reports_error(tk):
         c.stats()
     assert e.value.status == 9
     c.close()
+
+
+# ------------------------------------------------------------------------------ fused dense step 4
+@pytest.mark.parametrize("m,n", [(2, 4), (4, 2), (1, 8)])
+def test_hitopk_fused_dense_step4_replicated_decompress(tk, m, n):
+    """HiTopKComm's dense step 4 fused into step 3's accumulation (Alg. 2 l.15-23): GPU (i, j)
+    decompresses its column-gathered pairs once and writes segment j into the out buffer of every GPU
+    of its node (tk_decompress_replicated - on a node the replicas are the peers' CUDA-IPC mapped
+    outs); after all n positions ran, every GPU's out must equal the oracle's aggregate bit for bit."""
+    d, rho, N = 400_000, 0.001, 10
+    P, L = m * n, 400_000 // n
+    ctxs = [tk.Context(d, rho=rho, n_iters=N, nranks=P, rank=p, group_size=n, seed=8, loopback=True) for p in range(P)]
+    kt = ctxs[0].k
+    grads = [gradgen.gradient(d, "G", cfg=95, rank=p) for p in range(P)]
+    res = [np.zeros(L, np.float32) for _ in range(P)]
+    ref = oracle.hitopk_step(grads, res, m, n, rho, N, seed=8)
+    gd = [_dev(g) for g in grads]
+    chunks = {}
+    for i in range(m):
+        for j in range(n):
+            c = ctxs[i * n + j]
+            chunk = torch.empty(c.chunk_words, dtype=torch.int32, device="cuda")
+            c.compress_segment([gd[i * n + q][j * L:(j + 1) * L] for q in range(n)], _dev(res[i * n + j]),
+                               idx=chunk[:kt], val=chunk[kt:].view(torch.float32))
+            chunks[i * n + j] = chunk
+    for i in range(m):  # node i: n output buffers, filled by the n positions' replicated decompressions
+        outs = [torch.full((d,), float("nan"), device="cuda") for _ in range(n)]
+        for j in range(n):
+            col = torch.cat([chunks[a * n + j] for a in range(m)])
+            ctxs[i * n + j].decompress_replicated(col, [o[j * L:(j + 1) * L] for o in outs], nchunks=m)
+        for q in range(n):
+            assert np.array_equal(_bits(outs[q]), ref.out.view(np.uint32)), (i, q)
+    for c in ctxs:
+        c.close()
