@@ -36,6 +36,9 @@ def main():
     ap.add_argument("--sgd", type=float, default=0.0, help="also run Eq. 1's fused update with this lr")
     ap.add_argument("--zero-copy", action="store_true", help="write g into the context's input buffer")
     ap.add_argument("--bucket", action="store_true", help="drive the step through tk.Bucket (3 layer views)")
+    ap.add_argument("--symmetric", action="store_true",
+                    help="g and out in tk_alloc_symmetric buffers (in-place step 1, fused dense step 4)")
+    ap.add_argument("--no-ef", action="store_true", help="error feedback off")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
 
@@ -52,7 +55,8 @@ def main():
     log("uid ok")
     n = a.group_size
     kw = dict(n_iters=a.n_iters, nranks=ws, rank=rank, group_size=n, seed=99, uid=uid, step4=a.step4,
-              rs_mode=a.rs_mode, ag_mode=a.ag_mode, device=local, select=a.select, wire=a.wire)
+              rs_mode=a.rs_mode, ag_mode=a.ag_mode, device=local, select=a.select, wire=a.wire,
+              error_feedback=not a.no_ef)
     bucket = None
     if a.bucket:  # the same flat gradient, seen as three layers of one bucket (reading Q32)
         q = a.dim // 3
@@ -68,6 +72,8 @@ def main():
     ok = True
     r_ref = [np.zeros(L, np.float32) for _ in range(ws)]
     inbuf = ctx.input_buffer() if a.zero_copy else None
+    sym_g = [ctx.alloc_symmetric(a.dim) for _ in range(2)] if a.symmetric else None  # alternate between two
+    sym_out = ctx.alloc_symmetric(a.dim) if a.symmetric else None
     w_ref = gradgen.gradient(a.dim, "G", cfg=41)
     wd = torch.from_numpy(w_ref.copy()).cuda()
     for step in range(a.steps):
@@ -75,6 +81,9 @@ def main():
         if inbuf is not None:
             inbuf.copy_(g)
             g = inbuf
+        if sym_g is not None:
+            sym_g[step % 2].copy_(g)
+            g = sym_g[step % 2]
         gat = torch.empty(chunks * ctx.chunk_words, dtype=torch.int32, device="cuda")
         if bucket is not None:
             for (o, cnt, _), view in zip(bucket.layout, bucket.grads):
@@ -85,7 +94,7 @@ def main():
             out = torch.empty(a.dim, dtype=torch.float32, device="cuda")
             ctx.step_sgd(g, r, wd, a.sgd, out=out, gathered=gat)
         else:
-            out = ctx.step(g, r, gathered=gat)
+            out = ctx.step(g, r if not a.no_ef else None, out=sym_out, gathered=gat)
         torch.cuda.synchronize()
         log("step", step, "done")
         outs = [torch.empty_like(out) for _ in range(ws)]
@@ -101,19 +110,19 @@ def main():
             grads = [gradgen.gradient(a.dim, a.dist, cfg=40, rank=p, step=step) for p in range(ws)]
             if n == 1:
                 ref = oracle.flat_step(grads, r_ref, a.rho, a.n_iters, seed=99, step=step, selector=a.select,
-                                       wire=a.wire)
+                                       wire=a.wire, error_feedback=not a.no_ef)
                 ref_gat = [ref.gathered] * ws
             else:
                 ref = oracle.hitopk_step(grads, r_ref, ws // n, n, a.rho, a.n_iters, seed=99, step=step,
-                                         selector=a.select, wire=a.wire)
+                                         selector=a.select, wire=a.wire, error_feedback=not a.no_ef)
                 ref_gat = [ref.column_gathered[p % n] for p in range(ws)]
             rec = {"step": step}
             rec["out_equal"] = [bool(np.array_equal(o.cpu().numpy().view(np.uint32), ref.out.view(np.uint32)))
                                 for o in outs]
             rec["gathered_equal"] = [bool(np.array_equal(gg.cpu().numpy().view(np.uint32), ref_gat[p]))
                                      for p, gg in enumerate(gats)]
-            rec["residual_equal"] = [bool(np.array_equal(rr.cpu().numpy().view(np.uint32),
-                                                         ref.per_rank[p].residual.view(np.uint32)))
+            rec["residual_equal"] = [a.no_ef or bool(np.array_equal(rr.cpu().numpy().view(np.uint32),
+                                                                    ref.per_rank[p].residual.view(np.uint32)))
                                      for p, rr in enumerate(rs)]
             if a.sgd:
                 w_ref = oracle.sgd_update(w_ref, ref.out, a.sgd)
@@ -124,7 +133,8 @@ def main():
             rec["nnz_out"] = int(np.count_nonzero(ref.out))
             ok = ok and all(rec["out_equal"]) and all(rec["gathered_equal"]) and all(rec["residual_equal"])
             results.append(rec)
-            r_ref = [ref.per_rank[p].residual for p in range(ws)]
+            if not a.no_ef:
+                r_ref = [ref.per_rank[p].residual for p in range(ws)]
         dist.barrier()
     if rank == 0:
         with open(a.out, "w") as f:

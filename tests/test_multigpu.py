@@ -112,3 +112,26 @@ def test_bucketed_step_multi_gpu(P, n, tmp_path):
     """the bucketed multi-tensor step (reading Q32): three layer views of one bucket,
     flat or HiTopKComm (whose bucket gradient is libtk's peer-visible input buffer)"""
     _run(P, tmp_path, dim=8 * 131_076 if n > 1 else 1_000_003, rho=0.001, group_size=n, bucket=True, steps=3)
+
+
+@pytest.mark.parametrize("P,n,step4", [(2, 2, "dense"), (4, 4, "dense"), (4, 2, "dense"), (4, 2, "sparse"),
+                                       (8, 4, "dense"), (8, 2, "dense")])
+def test_hitopk_symmetric_buffers(P, n, step4, tmp_path):
+    """g and out in tk_alloc_symmetric buffers: the ordered reduce-scatter reads the peers' gradients
+    in place (no copy-in) and the dense step 4 is fused into the decompression (NVLink replica stores
+    into every node peer's out, then a row barrier) - Alg. 2 bit for bit, five steps"""
+    _run(P, tmp_path, dim=8 * 131_076, rho=0.001, group_size=n, step4=step4, symmetric=True, steps=5)
+
+
+@pytest.mark.parametrize("P,n,step4", [(2, 2, "dense"), (4, 2, "sparse")])
+def test_hitopk_no_error_feedback(P, n, step4, tmp_path):
+    """HiTopKComm with the ordered reduce-scatter and error feedback off (the peer sum is stored to a
+    segment scratch; round 1 crashed here)"""
+    _run(P, tmp_path, dim=8 * 131_076, rho=0.001, group_size=n, step4=step4, no_ef=True, steps=3)
+
+
+@pytest.mark.parametrize("P,n", [(4, 2), (4, 4), (8, 4), (8, 2)])
+def test_hitopk_c4_full_size_symmetric(P, n, tmp_path):
+    """BASELINE config 4 at full size with symmetric buffers, 4 steps (the EF-pass compaction of the
+    peer-sum kernel from step 1 on)"""
+    _run(P, tmp_path, dim=25_600_000, rho=0.001, group_size=n, symmetric=True, steps=4)

@@ -1,8 +1,23 @@
-set -x
-timeout 1200 python -m pytest tests/test_multigpu.py -x -q > gpurun_out/mgpu_tests.log 2>&1; echo "mgpu tests rc=$?"; tail -3 gpurun_out/mgpu_tests.log
-for N in 2 4; do
-  timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2950$N bench.py --gpus $N --steps 100 --warmup 10 > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err; echo "bench n=$N rc=$?"
-  timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2951$N bench.py --gpus $N --steps 100 --warmup 10 --ag-mode nccl --no-e2e > gpurun_out/bench_n${N}_nccl.json 2> gpurun_out/bench_n${N}_nccl.err; echo "bench nccl n=$N rc=$?"
+#!/bin/bash
+# multi-GPU pass (run with gpurun --gpus 4): multi-GPU parity tests, benches at P = 2 / 4 (flat and
+# HiTopKComm), and a soak of the HiTopKComm peer-sum kernel with the EF-pass compaction
+mkdir -p gpurun_out
+NG=$(nvidia-smi -L | wc -l)
+timeout 1500 python -m pytest -q -m gpu tests/test_multigpu.py ${PYT_K:+-k "$PYT_K"} > gpurun_out/pytest_mgpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_mgpu.log
+tr() { python -m torch.distributed.run --nnodes=1 --nproc-per-node $1 --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 1000)) bench.py --gpus $1 "${@:2}"; }
+run() { name=$1; shift; timeout 600 "$@" > gpurun_out/bench_$name.json 2> gpurun_out/bench_$name.err; echo "bench $name rc=$?"; }
+[ -z "$NO_BENCH" ] && {
+run n2 tr 2 --steps 30 --warmup 5 --no-e2e
+run n4 tr 4 --steps 30 --warmup 5 --no-e2e
+run h22_dense tr 4 --group-size 2 --steps 30 --warmup 5 --no-e2e
+run h22_sparse tr 4 --group-size 2 --step4 sparse --steps 30 --warmup 5 --no-e2e
+run h14_dense tr 4 --group-size 4 --steps 30 --warmup 5 --no-e2e
+run h14_sparse tr 4 --group-size 4 --step4 sparse --steps 30 --warmup 5 --no-e2e
+run h22_dense_r1e2 tr 4 --group-size 2 --rho 0.01 --steps 30 --warmup 5 --no-e2e
+run h14_sparse_r1e2 tr 4 --group-size 4 --rho 0.01 --step4 sparse --steps 30 --warmup 5 --no-e2e
+}
+[ -n "$SOAK" ] && for i in $(seq 1 $SOAK); do
+  timeout 300 bash -c "$(declare -f tr); tr 4 --group-size 4 --step4 sparse --steps 100 --warmup 5 --no-e2e --no-cpu-baseline" > gpurun_out/soak_$i.json 2> gpurun_out/soak_$i.err; echo "soak 1x4 sparse $i rc=$?"
+  timeout 300 bash -c "$(declare -f tr); tr 4 --group-size 2 --steps 100 --warmup 5 --no-e2e --no-cpu-baseline" > gpurun_out/soak2_$i.json 2> gpurun_out/soak2_$i.err; echo "soak 2x2 dense $i rc=$?"
 done
-timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29520 bench.py --gpus 4 --steps 50 --warmup 5 --group-size 2 --no-e2e > gpurun_out/bench_h22.json 2> gpurun_out/bench_h22.err; echo "bench hitopk rc=$?"
-timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29521 bench.py --gpus 4 --steps 50 --warmup 5 --group-size 4 --step4 sparse --no-e2e > gpurun_out/bench_h14s.json 2> gpurun_out/bench_h14s.err; echo "bench hitopk14s rc=$?"
+true
