@@ -145,6 +145,7 @@ SearchParams search_params(const tk_ctx* c) {
   sp.W = c->W;
   sp.S = c->S;
   sp.R = c->R;
+  sp.fold = (uint64_t)c->R * 8 >= (uint64_t)c->W * 7 ? 1u : 0u;
   sp.rank = c->rank;
   sp.rand_mode = c->cfg.rand_mode;
   sp.seed = c->cfg.seed;
@@ -312,14 +313,14 @@ tk_status plan_launches(tk_ctx* c) {
 #endif
   const uint64_t per_cta = (uint64_t)WARPS * TK_MIN_UNITS_PER_WARP;
   c->grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sms * occ, (rounds + per_cta - 1) / per_cta));
-  c->grid = std::min<uint32_t>(c->grid, 4096);  // stats_root folds <= 4096 CTA partials
+  c->grid = std::min<uint32_t>(c->grid, 4096 / WARPS);  // stats_root folds <= 4096 run sums (R <= W)
   c->W = c->grid * WARPS;
   uint64_t upw = 1;  // ef phase: aligned power-of-two run of units per warp covering the vector
   while ((uint64_t)c->W * upw < rounds) upw <<= 1;
   c->units_per_warp = (uint32_t)upw;
   c->S = upw * ROUND;  // count / select slabs = the ef phase's warp runs (acc is re-read from L2)
   c->R = (uint32_t)((rounds + upw - 1) / upw);
-  TK_TRY(dev_alloc(c, &c->cta_sum, c->grid));  // one partial sum per CTA
+  TK_TRY(dev_alloc(c, &c->cta_sum, c->W));  // one partial sum per run (R <= W)
   TK_TRY(dev_alloc(c, &c->cta_max, c->grid));
   TK_TRY(dev_alloc(c, &c->cta_cls, 4 * (size_t)c->grid));
   TK_TRY(dev_alloc(c, &c->cta_suffix, (size_t)c->grid * HIST_BINS));

@@ -131,17 +131,26 @@ struct SearchParams {
   uint32_t W;        // warp slabs (= gridDim.x * WARPS of the count / select launches)
   uint64_t S;        // slab length (one run of units_per_warp 512-element units)
   uint32_t R;        // runs: ceil(n / S) <= W
+  uint32_t fold;     // 1: warp gw owns run gw and each CTA folds its 8 runs (R >= 7/8 W); 0: balanced map
   uint32_t rank;
   uint32_t rand_mode;
   uint64_t seed;
 };
 
-// Warp -> run map: run j (elements [j*S, (j+1)*S)) belongs to warp j; the W - R warps past the end
-// are idle.  (Spreading the idle warps evenly over the CTAs was measured: it moves the last CTA's
-// end of the EF pass by only 0.5 us - the spread comes from the memory system, not the partition -
-// and it breaks the CTA-level fold of the canonical tree, which then costs more at the root.)
+// Warp -> run map (monotone, balanced over the CTAs): CTA b owns runs [floor(b*R/G), floor((b+1)*R/G))
+// - 0..8 consecutive runs - on its first warps; run j covers elements [j*S, (j+1)*S).  The runs must
+// stay aligned power-of-two blocks of units for the canonical tree (Q3), so R = ceil(n/S) < W in
+// general; leaving the W - R idle warps all in the last CTAs would idle whole SMs (measured: 2048 of
+// 3552 warps busy at d = 2^27 ran the EF pass 2x slower), so they are spread over the CTAs instead.
+// Each warp's subtree goes to run_sum[j]; stats_root folds the R run sums.
 __device__ __forceinline__ int32_t warp_run_of(const SearchParams& sp, uint32_t gw) {
-  return gw < sp.R ? (int32_t)gw : -1;
+  // when almost every warp has a run (R >= 7/8 W, e.g. C2: 3125 / 3552) the identity map is kept:
+  // each CTA's 8 runs are then one aligned subtree it folds itself, and stats_root reads only the
+  // G CTA partials (measured: ~1 us faster at the root, and the idle warps cost ~0.5 us)
+  if (sp.fold) return gw < sp.R ? (int32_t)gw : -1;
+  const uint32_t G = sp.W / WARPS, b = gw / WARPS, w = gw % WARPS;
+  const uint32_t j0 = b * sp.R / G, j1 = (b + 1) * sp.R / G;  // W * R < 2^32
+  return j0 + w < j1 ? (int32_t)(j0 + w) : -1;
 }
 
 // Compacted entries of the first count pass: warp w keeps, in ascending index order, every
@@ -709,8 +718,8 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
                                          uint32_t* __restrict__ cta_ent) {
   EfStage& es = g_es;
   constexpr bool STORE = EF || NP > 0;
-  __shared__ double s_ws[WARPS];
   __shared__ uint32_t s_wm[WARPS];
+  __shared__ double s_ws[WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t n = sp.n;
   const uint32_t gw = blockIdx.x * WARPS + warp;
@@ -847,7 +856,10 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   while ((1u << top) < units_per_warp) ++top;
   mx = __reduce_max_sync(0xffffffffu, mx);
   if (lane == 0) {
-    s_ws[warp] = run >= 0 ? stk[top] : 0.0;  // this run's aligned subtree of the canonical tree
+    // this run's aligned subtree of the canonical tree: to run_sum (balanced map) or, folded with
+    // the CTA's other 7 runs, to run_sum[blockIdx.x] (identity map)
+    if (!sp.fold && run >= 0) run_sum[run] = stk[top];
+    s_ws[warp] = run >= 0 ? stk[top] : 0.0;
     s_wm[warp] = mx;
     es.n[warp] = cmp_on ? ncomp : 0u;
     es.in_smem[warp] = in_smem ? 1u : 0u;
@@ -862,9 +874,9 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) te += es.n[w];
     cta_ent[blockIdx.x] = te;
-    // the CTA's 8 runs form an aligned subtree (the CTA owns runs [8b, 8b + 8))
-    run_sum[blockIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(s_ws[0], s_ws[1]), __dadd_rn(s_ws[2], s_ws[3])),
-                                    __dadd_rn(__dadd_rn(s_ws[4], s_ws[5]), __dadd_rn(s_ws[6], s_ws[7])));
+    if (sp.fold)
+      run_sum[blockIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(s_ws[0], s_ws[1]), __dadd_rn(s_ws[2], s_ws[3])),
+                                      __dadd_rn(__dadd_rn(s_ws[4], s_ws[5]), __dadd_rn(s_ws[6], s_ws[7])));
     uint32_t m = s_wm[0];
 #pragma unroll
     for (int w = 1; w < WARPS; ++w) m = max(m, s_wm[w]);
@@ -879,37 +891,56 @@ template <int SEL>
 __device__ __forceinline__ void stats_root(const double* __restrict__ run_sum, const uint32_t* __restrict__ cta_max,
                                            const uint32_t* __restrict__ cta_ent, const SearchParams& sp, Ctrl* sc,
                                            uint64_t step) {
-  // the CTA partials, zero-padded to Rp = 2^j >= THREADS leaves (extra zero leaves never change a
-  // pairwise sum of non-negatives, Q3): thread t folds its G consecutive leaves (binary-counter
-  // stack), the warp's 32 threads by xor shuffles, the 8 warps in thread 0 - the same pairs as the
-  // recursive definition
+  // Leaves: the G CTA partials (identity map, sp.fold) or the R run subtrees (balanced map),
+  // zero-padded to Lp = 2^j >= 256 leaves (extra zero leaves never change a pairwise sum of
+  // non-negatives, Q3); <= 4096 of them (plan_launches).  Folded in the canonical pairs:
+  //   fold: lane l of warp w holds its Lp/256 consecutive leaves (levels 1..), then xor shuffles;
+  //   runs: row q of 32 consecutive leaves per warp, loaded coalesced (lane l: leaf q*32 + l),
+  //         reduced by xor shuffles (levels 1-5), then the rows pairwise;
+  // then thread 0 folds the 8 warps.
   __shared__ double s_v[WARPS];
   __shared__ uint32_t s_m[WARPS], s_n[WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t Rp = THREADS;
-  while (Rp < gridDim.x) Rp <<= 1;
-  const uint32_t G = Rp / THREADS;  // leaves (CTA partials) per thread
+  const uint32_t nl = sp.fold ? gridDim.x : sp.R;
+  uint32_t Lp = THREADS;
+  while (Lp < nl) Lp <<= 1;
+  const uint32_t G = Lp / THREADS;  // 1..16, a power of two
   uint32_t m2 = 0, ne = 0;
   for (uint32_t b = tid; b < gridDim.x; b += THREADS) {
     m2 = max(m2, __ldcg(cta_max + b));
     ne += __ldcg(cta_ent + b);
   }
-  // G <= 16 consecutive leaves per thread (grids up to 4096 CTAs), loaded together, then
-  // folded pairwise (G is a power of two: the loops below visit exactly the pairs of a G-leaf tree)
   double lv[16];
+  if (sp.fold) {
+    const uint32_t l0 = (uint32_t)tid * G;
 #pragma unroll
-  for (uint32_t q = 0; q < 16; ++q) {
-    const uint32_t li = tid * G + q;
-    lv[q] = (q < G && li < gridDim.x) ? __ldcg(run_sum + li) : 0.0;
+    for (uint32_t q = 0; q < 16; ++q) lv[q] = (q < G && l0 + q < nl) ? __ldcg(run_sum + l0 + q) : 0.0;
+#pragma unroll
+    for (uint32_t w = 1; w < 16; w <<= 1)
+#pragma unroll
+      for (uint32_t q = 0; q < 16; q += 2 * w)
+        if (w < G) lv[q] = __dadd_rn(lv[q], lv[q + w]);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) lv[0] = __dadd_rn(lv[0], __shfl_xor_sync(0xffffffffu, lv[0], off));
+  } else {
+#pragma unroll
+    for (uint32_t q = 0; q < 16; ++q) {
+      const uint32_t li = warp * (Lp / WARPS) + q * 32 + lane;
+      lv[q] = (q < G && li < nl) ? __ldcg(run_sum + li) : 0.0;
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < 16; ++q)
+      if (q < G) {
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) lv[q] = __dadd_rn(lv[q], __shfl_xor_sync(0xffffffffu, lv[q], off));
+      }
+#pragma unroll
+    for (uint32_t w = 1; w < 16; w <<= 1)
+#pragma unroll
+      for (uint32_t q = 0; q < 16; q += 2 * w)
+        if (w < G) lv[q] = __dadd_rn(lv[q], lv[q + w]);
   }
-#pragma unroll
-  for (uint32_t w = 1; w < 16; w <<= 1)
-#pragma unroll
-    for (uint32_t q = 0; q < 16; q += 2 * w)
-      if (w < G) lv[q] = __dadd_rn(lv[q], lv[q + w]);
-  double v = lv[0];
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+  const double v = lv[0];
   m2 = __reduce_max_sync(0xffffffffu, m2);
   ne = __reduce_add_sync(0xffffffffu, ne);
   if (lane == 0) { s_v[warp] = v; s_m[warp] = m2; s_n[warp] = ne; }
@@ -1412,7 +1443,7 @@ struct Fused {
                              // without EF), nullptr (acc = g)
   const float* acc;          // the vector MSTopK reads: accw or g
   uint32_t units_per_warp;   // ef phase: aligned power-of-two run of 512-element units per warp
-  double* cta_sum;           // [grid] ef partials: one aligned canonical-tree subtree per CTA
+  double* cta_sum;           // [R] ef partials: one aligned canonical-tree subtree per run
   uint32_t* cta_max;         // [grid]
   uint32_t* wcnt;            // [npass * TMAX][W] per-warp-slab trial counts
   uint32_t* totals;          // [npass][16] global trial counts
