@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--no-symmetric", action="store_true",
                     help="HiTopKComm: plain gradient / output tensors (copy-in, NCCL row all-gather)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the extra single-GPU configurations")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu: no soak, no e2e, no cpu baseline")
     return ap.parse_args()
@@ -363,6 +364,88 @@ def nvlink_report(a, stages, P, n, L, k, t_step_ms, cw):
     return rep
 
 
+def extra_configs(a, tk, stream, gs, dev):
+    """Single-GPU context numbers measured after the timed region (device time, CUDA events on the
+    context stream, fresh gradients): BASELINE config 1 (d = 1M, EF off, tk_compress only, from a
+    CUDA graph so the host's launch cost is excluded); the first call of a fresh context (no
+    prediction) and a forced restart (the gradient scale jumps x1000); the C2 step with the layered
+    ResNet-like profile, with the prose search (F3) and with the exact selector (F1)."""
+    import torch
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def steps_us(ctx, bufs, n, r):
+        for i in range(3):
+            ctx.step(bufs[i % len(bufs)], r)
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for i in range(n):
+            ctx.step(bufs[i % len(bufs)], r)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / n
+
+    res = {}
+    with torch.cuda.stream(stream):
+        # C1
+        d1 = 1_000_000
+        c1 = tk.Context(d1, rho=a.rho, n_iters=a.n_iters, error_feedback=False, stream=stream, device=dev)
+        g1 = [torch.randn(d1, device="cuda") for _ in range(16)]
+        idx = torch.empty(c1.k, dtype=torch.int32, device="cuda")
+        val = torch.empty(c1.k, device="cuda")
+        for i in range(40):
+            c1.compress(g1[i % 16], None, idx, val)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(16):
+                c1.compress(g1[i], None, idx, val)
+        graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(20):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res["C1_compress_us"] = e0.elapsed_time(e1) * 1e3 / 320
+        res["C1_phases_us"] = [round(x, 2) for x in c1.stats().phase_us]
+        c1.close()
+        del g1
+        # first call / restart at C2
+        c = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, stream=stream, device=dev)
+        r = torch.zeros(a.d, device="cuda")
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        c.step(gs[0], r)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res["C2_first_step_us"] = e0.elapsed_time(e1) * 1e3
+        for i in range(10):
+            c.step(gs[(i + 1) % len(gs)], r)
+        big = gs[0] * 1000.0
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        c.step(big, r)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res["C2_restart_step_us"] = e0.elapsed_time(e1) * 1e3
+        res["C2_restart_took_whole_vector_path"] = not c.stats().ef_compacted
+        c.close()
+        del big
+        # layered profile
+        gl = [torch.from_numpy(gradgen.gradient(a.d, "L", cfg=2, step=s_)).cuda() for s_ in range(4)]
+        c = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, stream=stream, device=dev)
+        res["C2_dist_L_step_us"] = steps_us(c, gl, 20, torch.zeros(a.d, device="cuda"))
+        c.close()
+        del gl
+        for sel in ("prose", "exact"):
+            c = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, stream=stream, device=dev, select=sel)
+            res[f"C2_{sel}_step_us"] = steps_us(c, gs, 20, torch.zeros(a.d, device="cuda"))
+            c.close()
+    res["note"] = ("device time per call / step (CUDA events, fresh gradients); C1 replays 16 tk_compress calls "
+                   "per CUDA graph; prose = TK_SELECT_PROSE (P:148), exact = TK_SELECT_EXACT (Eq. 2)")
+    return res
+
+
 def log(*x):
     print(f"[bench {time.strftime('%H:%M:%S')}]", *x, file=sys.stderr, flush=True)
 
@@ -569,6 +652,11 @@ def main():
         recall = {"index_recall": hit / k, "magnitude_ratio": sel["mstopk"][1] / sel["exact"][1],
                   "note": "MSTopK vs exact top-k (Eq. 2) on the step-0 gradient, both on the GPU, EF off"}
 
+    extra = None
+    if rank == 0 and P == 1 and n == 1 and not a.ncu and not a.no_extra:
+        extra = extra_configs(a, tk, stream, gs, local)
+        log("extra configurations done")
+
     cpu = None
     if rank == 0 and P == 1 and not a.no_cpu_baseline and not a.ncu:
         cpu = cpu_baseline(a, P)
@@ -588,7 +676,7 @@ def main():
                                  f"{12 * a.d / 1e6:.0f} MB per rank per step vs 126 MB L2; no explicit flush"},
                 "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "stages": stages, "recall_vs_exact": recall, "nvlink": nvlink,
-                "dense_allreduce_comparator": allreduce}
+                "dense_allreduce_comparator": allreduce, "extra_configs": extra}
         emit(line)
     ctx.close()
     if ws > 1:

@@ -46,6 +46,11 @@ struct tk_ctx {
   uint32_t* dev_err = nullptr;        // device word: the fused all-gather's wait timed out (sticky)
   uint32_t timeout_sticky = 0;
   uint64_t timeout_ns = 0;
+#ifdef TK_NO_PDL  // experiment builds
+  bool pdl = false;
+#else
+  bool pdl = true;                    // programmatic dependent launch (falls back when refused)
+#endif
   int lev_sched[NMAX];
   uint32_t units_per_warp = 1;        // ef phase: aligned power-of-two run of 512-element units per warp
   uint32_t* cta_cls = nullptr;        // [4][grid] per-CTA class counts, entries
@@ -126,6 +131,41 @@ tk_status check_launch(tk_ctx* c, const char* what) {
   c->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(c, TK_ERR_CUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  return TK_OK;
+}
+
+// Launch one of libtk's kernels on the context stream with programmatic dependent launch (the grid
+// may be scheduled while the previous kernel drains; every kernel opens with griddepcontrol.wait),
+// cooperatively for k_compress.  A driver that refuses the attribute gets a plain launch.
+tk_status launch(tk_ctx* c, const void* kern, dim3 grid, size_t smem, void** args, bool cooperative) {
+  if (c->pdl) {
+    cudaLaunchAttribute at[2];
+    unsigned na = 0;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    if (cooperative) {
+      at[na].id = cudaLaunchAttributeCooperative;
+      at[na].val.cooperative = 1;
+      ++na;
+    }
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    if (cudaLaunchKernelExC(&cfg, kern, args) == cudaSuccess) return TK_OK;
+    (void)cudaGetLastError();
+    c->pdl = false;  // not supported here: plain launches from now on
+  }
+  if (cooperative) {
+    TK_CUDA(c, cudaLaunchCooperativeKernel(kern, grid, dim3(THREADS), args, smem, c->stream));
+  } else {
+    TK_CUDA(c, cudaLaunchKernel(kern, grid, dim3(THREADS), args, smem, c->stream));
+  }
   return TK_OK;
 }
 
@@ -222,7 +262,7 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   const void* kern = compress_kernel(ef, np, c->cfg.select);
   if (!kern) return fail(c, TK_ERR_CONFIG, "unsupported peer count %d", np);
   void* args[] = {&f};
-  TK_CUDA(c, cudaLaunchCooperativeKernel(kern, dim3(c->grid), dim3(THREADS), args, 0, c->stream));
+  TK_TRY(launch(c, kern, dim3(c->grid), 0, args, true));
   if (c->debug_check) {
     k_check_sel<<<1, 1024, 0, c->stream>>>(idx, c->k, c->L, (uint32_t)c->rank, (uint32_t)c->step, 0u);
     TK_TRY(check_launch(c, "k_check_sel"));
@@ -251,9 +291,12 @@ tk_status decompress_impl(tk_ctx* c, const Src& src, uint32_t nchunks, uint64_t 
         k_check_sel<<<1, 1024, 0, c->stream>>>(src.g + (size_t)p * c->cw, kk, len, (uint32_t)c->rank, (uint32_t)c->step,
                                                1u + p);
   }
-  k_decompress<Src><<<grid, THREADS, sizeof(uint32_t) * nchunks, c->stream>>>(src, nchunks, kk, len, nt, per, out,
-                                                                               plain_out, w, lr, c->cw,
-                                                                               c->cfg.wire == TK_WIRE_F16 ? 1u : 0u, rp);
+  const uint32_t w16 = c->cfg.wire == TK_WIRE_F16 ? 1u : 0u;
+  const uint64_t cw = c->cw;
+  void* args[] = {const_cast<Src*>(&src), &nchunks, &kk, &len, const_cast<uint32_t*>(&nt), const_cast<uint32_t*>(&per),
+                  &out, &plain_out, &w, &lr, const_cast<uint64_t*>(&cw), const_cast<uint32_t*>(&w16), &rp};
+  TK_TRY(launch(c, reinterpret_cast<const void*>(&k_decompress<Src>), dim3(grid), sizeof(uint32_t) * nchunks, args,
+                false));
   TK_TRY(check_launch(c, "k_decompress"));
   mark(c, TK_STAGE_DECOMPRESS);
   return TK_OK;

@@ -1562,6 +1562,9 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   __shared__ uint32_t s_base[2];
   __shared__ uint32_t s_ne[WARPS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // programmatic dependent launch: this grid may have been launched while the previous kernel on
+  // the stream was finishing; nothing it wrote (nor anything before it) is read before this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ uint64_t bar_t;  // thread 0: target of the next grid barrier (shared: keeps it out of registers)
   if (tid == 0) bar_t = grid_sync_base(f.bar);
   if (lane == 0) g_es.run[warp] = warp_run_of(f.sp, blockIdx.x * WARPS + warp);
@@ -2011,6 +2014,9 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   }
   uint32_t b1 = s_base[0], b2 = s_base[1];
   for (int w = 0; w < warp; ++w) { b1 += s_w[0][w]; b2 += s_w[1][w]; }
+  // the next kernel on the stream (the decompression) may start launching: its CTAs wait for this
+  // grid's completion (griddepcontrol.wait) before reading anything
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- A7-A8: selection, compaction, residual write-back ----
   {
     SelOut so;
@@ -2119,6 +2125,10 @@ __global__ void __launch_bounds__(THREADS) k_decompress(const Src src, uint32_t 
   __shared__ __align__(16) float s_tile[TILE];
   extern __shared__ uint32_t s_cur[];  // [nchunks] per-rank cursors
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // programmatic dependent launch (see k_compress): wait for the previous grid, then let the next
+  // one start launching
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t t0 = blockIdx.x * tiles_per_cta;
   const uint32_t t1 = min(ntiles, t0 + tiles_per_cta);
   if (t0 >= t1) return;
