@@ -13,6 +13,8 @@ Distributions (the paper states none: "different length of vectors", P:377
 * ``"G"``  iid N(0,1) fp32 (default).
 * ``"L"``  layered, ResNet-like: d cut into 161 contiguous blocks (ResNet-50's layer
   count) at seeded sorted uniform cut points; block scale 10**U(-4,0) times N(0,1).
+  The blocks and scales depend on (cfg, rank) only - the same network at every step - and
+  the N(0,1) noise on the step.
 * ``"H"``  Laplace(0,1) (heavy tailed).
 * edge cases (correctness only): ``"zero"``, ``"const"``, ``"spike"``, ``"ties8"``
   (8 magnitude levels, massive ties), ``"denorm"``, ``"signed_zero"``.
@@ -41,10 +43,13 @@ def gradient(d: int, dist: str = "G", cfg: int = 0, rank: int = 0, step: int = 0
         x = g.standard_normal(d, dtype=np.float32)
     elif dist == "L":
         x = g.standard_normal(d, dtype=np.float32)
+        # the network (layer boundaries and per-layer scales) is the same at every step of a rank,
+        # as in training; only the noise is drawn per step
+        gl = rng_for(cfg, rank, 1 << 40)  # a step no caller uses: the network's own stream
         nl = min(N_LAYERS, max(1, d))
-        cuts = np.sort(g.integers(0, d + 1, size=nl - 1)) if nl > 1 else np.zeros(0, np.int64)
+        cuts = np.sort(gl.integers(0, d + 1, size=nl - 1)) if nl > 1 else np.zeros(0, np.int64)
         bounds = np.concatenate([[0], cuts, [d]]).astype(np.int64)
-        scales = (10.0 ** g.uniform(-4.0, 0.0, size=nl)).astype(np.float32)
+        scales = (10.0 ** gl.uniform(-4.0, 0.0, size=nl)).astype(np.float32)
         for li in range(nl):
             lo, hi = bounds[li], bounds[li + 1]
             if hi > lo:

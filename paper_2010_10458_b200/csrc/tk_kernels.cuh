@@ -1152,7 +1152,9 @@ __device__ __forceinline__ void hist_phase(const Ctrl* sc, const Compact cp, uin
     uint32_t b = 0;
 #pragma unroll 1
     for (int l = LEV - 1; l >= 0; --l) b += (a >= s_key[b + (1u << l) - 1]) ? (1u << l) : 0u;
-    atomicAdd(&s_h[b], 1u);
+    // warp-aggregated: the entries crowd into the few bins just above the compaction key
+    const uint32_t peers = __match_any_sync(__activemask(), b);
+    if ((__ffs(peers) - 1) == (threadIdx.x & 31)) atomicAdd(&s_h[b], (uint32_t)__popc(peers));
   };
   // a warp holds few entries in the EF-pass regime (~15 at C2): one per lane per iteration keeps
   // this once-per-launch code small (its instructions are fetched cold every launch)
@@ -1771,9 +1773,12 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       sc.prev_T = T;
       // next call's ef-phase compaction key: below T by half its last move if T rose (error
       // feedback grows the residual), else twice it, plus a margin
-      const uint32_t est = max(min(sc.prev_dT, 1u << 22), sc.mv_est / 2u);  // as for MSTopK's key2 below
+      // as for MSTopK's key2 below: twice the decaying maximum fall of T plus an eighth of its rise
+      const uint32_t fall = (P > 0u) ? (T < P ? P - T : 0u) : (1u << 21);
+      const uint32_t rise = (P > 0u && T > P) ? T - P : 0u;
+      const uint32_t est = max(min(fall, 1u << 22), sc.mv_est - sc.mv_est / 4u);
       sc.mv_est = est;
-      const uint32_t delta = min(1u << 22, 2u * est + (1u << 14));
+      const uint32_t delta = min(1u << 22, 2u * est + (1u << 14) + rise / 8u);
       sc.ef_key = T > delta ? T - delta : 0u;
     }
     __syncthreads();
@@ -1918,14 +1923,16 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
     const uint32_t K = sc.key2;
     if (sc.prov2 >= 0) {
       const uint32_t P = sc.prev_key2;
-      const uint32_t dk = (P > 0u) ? (K > P ? K - P : P - K) : (1u << 21);
-      // the margin below key2 covers twice the largest recent move (decaying by half per call):
-      // a prediction that fails costs a whole-vector restart (~20 us at C2), a generous margin
-      // only a few thousand more entries (measured: i.i.d. inputs without error feedback move key2
-      // both ways by ~20-60K ulps per call; with EF it mostly rises)
-      const uint32_t est = max(min(dk, 1u << 22), sc.mv_est / 2u);
+      // The margin below key2 covers twice the largest recent FALL of key2 (a decaying maximum,
+      // x3/4 per call) plus an eighth of this call's rise: a fall beyond it costs a whole-vector
+      // restart (~100-200 us at C2), a margin too generous costs entries (the histogram, prefix and
+      // selection work on them).  Measured: i.i.d. inputs without EF move key2 both ways by
+      // ~20-60K ulps per call; with EF it keeps rising (by up to ~1M ulps per call for heavy tails).
+      const uint32_t fall = (P > 0u) ? (K < P ? P - K : 0u) : (1u << 21);
+      const uint32_t rise = (P > 0u && K > P) ? K - P : 0u;
+      const uint32_t est = max(min(fall, 1u << 22), sc.mv_est - sc.mv_est / 4u);
       sc.mv_est = est;
-      const uint32_t margin = min(1u << 22, 2u * est + (1u << 14));
+      const uint32_t margin = min(1u << 22, 2u * est + (1u << 14) + rise / 8u);
       sc.ef_key = K > margin ? K - margin : 0u;
       sc.prev_key2 = K;
     } else {
