@@ -50,9 +50,15 @@ constexpr uint32_t NO_INDEX = 0xFFFFFFFFu;
 #else
 #define TK_DCHECK(cond, tag, a, b) do { } while (0)
 #endif
-// Global pass totals / histograms are replicated HREP times (copy = CTA index mod HREP) so the
-// CTAs' atomic adds spread over HREP addresses per bin; readers sum the copies.
-constexpr int HREP = 8;
+// Global pass totals / histograms can be replicated HREP times (copy = CTA index mod HREP) to spread
+// the CTAs' atomic adds over HREP addresses per bin; readers sum the copies.  One copy is fastest:
+// the histogram pass adds only its non-empty bins (C2: ~1e5 adds over ~450 bins), and every CTA then
+// reads the whole histogram after the barrier - measured at C2, 8 copies: 73.9 us per call, 4: 73.4,
+// 2: 72.4, 1: 71.8 (the read of 8 copies costs 2 us more than the contention it saves).
+#ifndef TK_HREP
+#define TK_HREP 1
+#endif
+constexpr int HREP = TK_HREP;
 // COUNT_HIST: up to HIST_LEV bisection levels (2^HIST_LEV - 1 candidate keys) per histogram pass
 constexpr int HIST_LEV = 10;
 constexpr int HIST_BINS = 1 << HIST_LEV;
@@ -490,10 +496,10 @@ __device__ __forceinline__ void finish_window(Ctrl* c, const SearchParams& sp) {
   c->need = (uint32_t)need;
   uint64_t r = 0;
   if (sp.rand_mode == 0) {
-    uint64_t h = sm64(sp.seed);
-    h = sm64(h ^ c->step);
-    h = sm64(h ^ (uint64_t)sp.rank);
-    h = sm64(h ^ 0ull);
+    // H = sm64(sm64(sm64(sm64(seed) ^ step) ^ rank) ^ 0), as a loop (one copy of the code)
+    uint64_t h = sp.seed;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) h = sm64(h ^ (q == 1 ? c->step : (q == 2 ? (uint64_t)sp.rank : 0ull)));
     r = __umul64hi(h, R);
   }
   c->rand = r;
@@ -884,13 +890,13 @@ __device__ __forceinline__ void ef_phase(const float* __restrict__ g, const Peer
   }
 }
 
-// Root of the canonical tree (every CTA computes it, identically, after the grid barrier):
-// the CTA partials zero-padded to Lp = 2^j >= THREADS leaves (extra zero leaves never change a
-// pairwise sum of non-negatives, Q3), then a-bar, u and the first pass's candidates.
-template <int SEL>
-__device__ __forceinline__ void stats_root(const double* __restrict__ run_sum, const uint32_t* __restrict__ cta_max,
-                                           const uint32_t* __restrict__ cta_ent, const SearchParams& sp, Ctrl* sc,
-                                           uint64_t step) {
+// Root of the canonical tree: the CTA partials (identity map) or the run subtrees (balanced map)
+// zero-padded to Lp = 2^j >= THREADS leaves (extra zero leaves never change a pairwise sum of
+// non-negatives, Q3), then a-bar, u and the first pass's candidates.  stats_fold reads the
+// partials and returns (S, u bits, entries) in thread 0.
+__device__ __forceinline__ void stats_fold(const double* __restrict__ run_sum, const uint32_t* __restrict__ cta_max,
+                                           const uint32_t* __restrict__ cta_ent, const SearchParams& sp, double& S_out,
+                                           uint32_t& m_out, uint32_t& t_out) {
   // Leaves: the G CTA partials (identity map, sp.fold) or the R run subtrees (balanced map),
   // zero-padded to Lp = 2^j >= 256 leaves (extra zero leaves never change a pairwise sum of
   // non-negatives, Q3); <= 4096 of them (plan_launches).  Folded in the canonical pairs:
@@ -906,6 +912,7 @@ __device__ __forceinline__ void stats_root(const double* __restrict__ run_sum, c
   while (Lp < nl) Lp <<= 1;
   const uint32_t G = Lp / THREADS;  // 1..16, a power of two
   uint32_t m2 = 0, ne = 0;
+#pragma unroll 2  // (grid <= 512 CTAs: both rounds' loads in flight together)
   for (uint32_t b = tid; b < gridDim.x; b += THREADS) {
     m2 = max(m2, __ldcg(cta_max + b));
     ne += __ldcg(cta_ent + b);
@@ -951,9 +958,28 @@ __device__ __forceinline__ void stats_root(const double* __restrict__ run_sum, c
                                __dadd_rn(__dadd_rn(s_v[4], s_v[5]), __dadd_rn(s_v[6], s_v[7])));
     uint32_t m = s_m[0], t = s_n[0];
     for (int w = 1; w < WARPS; ++w) { m = max(m, s_m[w]); t += s_n[w]; }
-    stats_finalize<SEL>(sc, sp, S, m, step);
-    sc->n_compacted = t;  // entries the ef phase kept (statistics)
+    S_out = S;
+    m_out = m;
+    t_out = t;
   }
+}
+
+// Root after the grid barrier: every CTA folds the partials itself and finalises its own control
+// block.  (Measured alternative: the CTA that arrives last folds and publishes the root through a
+// flag - 0.3 us slower at C2, the flag round trip costs more than the shared L2 reads it saves.)
+template <int SEL>
+__device__ __forceinline__ void stats_root(const double* __restrict__ run_sum, const uint32_t* __restrict__ cta_max,
+                                           const uint32_t* __restrict__ cta_ent, const SearchParams& sp, Ctrl* sc,
+                                           uint64_t step) {
+  __shared__ double s_S;
+  __shared__ uint32_t s_mt[2];
+  stats_fold(run_sum, cta_max, cta_ent, sp, s_S, s_mt[0], s_mt[1]);
+  TK_TRACE(10);
+  if (threadIdx.x == 0) {
+    stats_finalize<SEL>(sc, sp, s_S, s_mt[0], step);
+    sc->n_compacted = s_mt[1];  // entries the ef phase kept (statistics)
+  }
+  TK_TRACE(11);
   __syncthreads();
 }
 
@@ -1219,6 +1245,7 @@ __device__ __forceinline__ void hist_to_counts(const uint32_t* ghist, int lev, u
     for (int c = 0; c < HREP; ++c) v[q] += x[q][c];
     sum += v[q];
   }
+  TK_TRACE(14);
   uint32_t total;
   uint32_t acc = block_excl_scan(sum, s_w, total);
 #pragma unroll
@@ -1269,6 +1296,7 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
   const uint32_t gw = blockIdx.x * WARPS + warp;
   uint64_t lo, hi;
   warp_slab(sp, warp, lo, hi);
+  TK_TRACE(12);
   if (lo >= hi) return;
   const int32_t p1 = c->prov1, p2 = c->prov2;
   const int32_t key1 = (p1 >= 0) ? (int32_t)c->key1 : (int32_t)INF_BITS;
@@ -1314,26 +1342,24 @@ __device__ __forceinline__ void select_phase(const float* __restrict__ acc, cons
       const uint32_t excl = incl - packed;
       uint32_t q1 = b1 + (excl & 0xFFFFu);
       uint32_t q2 = b2 + (excl >> 16);
+      // one put_sel per element (this once-per-launch code is fetched cold: keep it small)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        if (fc1 & (1u << e)) {
-          const uint32_t after = (q2 > rnd) ? min(q2 - rnd, need) : 0u;
-          const uint32_t pos = q1 + after;
-          TK_DCHECK(pos < sp.k && ii[e] < sp.n, "sel-cap1", pos, ii[e]);
+        const uint32_t x1 = (fc1 >> e) & 1u, x2 = (fc2 >> e) & 1u;
+        uint32_t pos = 0xFFFFFFFFu;
+        if (x1) pos = q1 + ((q2 > rnd) ? min(q2 - rnd, need) : 0u);
+        else if (x2 && q2 >= rnd && q2 < rnd + need) pos = q1 + (q2 - rnd);
+        q1 += x1;
+        q2 += x2;
+        if (pos != 0xFFFFFFFFu) {
+          TK_DCHECK(pos < sp.k && ii[e] < sp.n, "sel-cap", pos, ii[e]);
           put_sel(so, pos, ii[e], __uint_as_float(bb[e]));
-          ++q1;
-        } else if (fc2 & (1u << e)) {
-          if (q2 >= rnd && q2 < rnd + need) {
-            const uint32_t pos = q1 + (q2 - rnd);
-            TK_DCHECK(pos < sp.k && ii[e] < sp.n, "sel-cap2", pos, ii[e]);
-            put_sel(so, pos, ii[e], __uint_as_float(bb[e]));
-          }
-          ++q2;
         }
       }
       b1 += tot & 0xFFFFu;
       b2 += tot >> 16;
     }
+    TK_TRACE(13);
     return;
   }
   const uint32_t* a32 = reinterpret_cast<const uint32_t*>(acc);
@@ -1993,6 +2019,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       // class counts of the CTAs before this one, from their published histogram suffixes: key1 /
       // key2 are candidates s1 / s2 of the single pass (prov = pass 0 * TMAX + s)
       const int s1 = sc.prov1, s2 = sc.prov2;
+#pragma unroll 2  // (grid <= 512 CTAs: both rounds' loads in flight together)
       for (uint32_t b = tid; b < blockIdx.x; b += THREADS) {
         const uint32_t* S = f.cta_suffix + (size_t)b * HIST_BINS;
         const uint32_t x1 = s1 >= 0 ? __ldcg(S + s1 + 1) : 0u;

@@ -39,3 +39,12 @@ for kind, name in ((0, "stamp"), (1, "arrive")):
         mn, md, mx = (np.median(v.min(1)) / 1e3, np.median(np.median(v, 1)) / 1e3, np.median(v.max(1)) / 1e3)
         late = np.bincount(v.argmax(1), minlength=G).argmax()
         print(f"  {name:6s} {slot:2d}: min {mn:7.2f} med {md:7.2f} max {mx:7.2f}  (latest CTA most often: {late})")
+# EF-pass arrival (barrier 1) by SM load: CTAs with a run (arrival > 5 us) per SM, and arrival percentiles
+arr = np.median(a[:, 1, 1, :], 0) / 1e3
+busy = arr > 5.0
+per_sm = np.bincount(smid, weights=busy.astype(float), minlength=smid.max() + 1)
+load = per_sm[smid]
+print("  ef arrivals of busy CTAs: p10 %.2f p50 %.2f p90 %.2f p99 %.2f max %.2f" % tuple(np.percentile(arr[busy], [10, 50, 90, 99, 100])))
+for nb in sorted(set(load[busy].astype(int))):
+    sel = busy & (load == nb)
+    print(f"  SMs with {nb} busy CTAs: {sel.sum()} CTAs, arrival p50 {np.median(arr[sel]):.2f} max {arr[sel].max():.2f}")
