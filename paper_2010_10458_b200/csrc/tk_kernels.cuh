@@ -485,24 +485,76 @@ __device__ __forceinline__ bool bracket_low_at_least(const Ctrl* c, double x) {
   return c->lo >= x;
 }
 
-// Alg. 1 l.27 window: R = len(iota2) - (k - k1) + 1 >= 1 (Q8, Q9); rand uniform on [0, R).
-__device__ __forceinline__ void finish_window(Ctrl* c, const SearchParams& sp) {
-  const uint64_t k1 = c->k1;
-  const uint64_t cnt2 = (c->prov2 >= 0) ? (uint64_t)c->k2 : sp.n;  // count(a >= thres2)
-  const uint64_t len2 = cnt2 - k1;
-  const uint64_t need = sp.k - k1;
-  const uint64_t R = len2 - need + 1;
-  c->len2 = len2;
-  c->need = (uint32_t)need;
-  uint64_t r = 0;
-  if (sp.rand_mode == 0) {
-    // H = sm64(sm64(sm64(sm64(seed) ^ step) ^ rank) ^ 0), as a loop (one copy of the code)
-    uint64_t h = sp.seed;
+// Alg. 1 l.27's random source (Q10): H = SplitMix64 chain over (seed, step, rank, 0); it does not
+// depend on the data, so each launch computes it once, off the critical path.
+__device__ __forceinline__ uint64_t window_hash(uint64_t seed, uint64_t step, uint32_t rank) {
+  // sm64(sm64(sm64(sm64(seed) ^ step) ^ rank) ^ 0), as a loop (one copy of the code)
+  uint64_t h = seed;
 #pragma unroll 1
-    for (int q = 0; q < 4; ++q) h = sm64(h ^ (q == 1 ? c->step : (q == 2 ? (uint64_t)sp.rank : 0ull)));
-    r = __umul64hi(h, R);
+  for (int q = 0; q < 4; ++q) h = sm64(h ^ (q == 1 ? step : (q == 2 ? (uint64_t)rank : 0ull)));
+  return h;
+}
+
+// Alg. 1 l.27 window: R = len(iota2) - (k - k1) + 1 >= 1 (Q8, Q9); rand uniform on [0, R):
+// floor(H * R / 2^64).  (k1, k2 as counts; k2 counts a >= thres2, n when thres2 was never set.)
+struct Window {
+  uint64_t len2, need, rand;
+};
+__device__ __forceinline__ Window window_of(uint64_t k1, uint64_t cnt2, const SearchParams& sp, uint64_t H) {
+  Window w;
+  w.len2 = cnt2 - k1;
+  w.need = sp.k - k1;
+  const uint64_t R = w.len2 - w.need + 1;
+  w.rand = (sp.rand_mode == 0) ? __umul64hi(H, R) : 0ull;
+  return w;
+}
+__device__ __forceinline__ void finish_window(Ctrl* c, const SearchParams& sp, uint64_t H) {
+  const Window w = window_of(c->k1, (c->prov2 >= 0) ? (uint64_t)c->k2 : sp.n, sp, H);
+  c->len2 = w.len2;
+  c->need = (uint32_t)w.need;
+  c->rand = w.rand;
+}
+
+// The selection's inputs straight from a histogram pass that resolves ALL N levels (the fast
+// search's single pass): every thread walks Alg. 1 l.8-21 over the pass's complete candidate
+// subtree (node m's count is tot[m-1]; right iff nnz > k) from the reset state (l.4-6) and keeps
+// only k1 / k2 and their candidates - the same decisions replay_levels takes, without its trial
+// log, thresholds and bracket, which block 0 fills in after the selection (the control block it
+// writes back is bit-identical).  ok: thres2 was set at or above the ef-phase key (the search was
+// exact, see k_compress).
+struct FastDecision {
+  int32_t s1, s2;      // candidate index of thres1 / thres2 (-1: never set)
+  uint32_t k1, k2;     // Alg. 1's k1, k2
+  uint32_t key1, key2;
+  Window w;
+  bool ok;
+};
+__device__ __forceinline__ FastDecision fast_walk(const Ctrl* c, const uint32_t* tot, int lev, const SearchParams& sp,
+                                                  uint32_t efk, uint64_t H) {
+  FastDecision d;
+  int m = 1 << (lev - 1), st = m >> 1;
+  d.k1 = 0u;
+  d.k2 = (uint32_t)sp.n;
+  d.s1 = -1;
+  d.s2 = -1;
+#pragma unroll 1
+  for (int l = 0; l < lev; ++l) {
+    const int s = m - 1;
+    const uint32_t nnz = tot[s];
+    if ((uint64_t)nnz > sp.k) {           // l.17-21
+      if (nnz < d.k2) { d.k2 = nnz; d.s2 = s; }
+      m += st;
+    } else {                              // l.11-15
+      if (nnz > d.k1) { d.k1 = nnz; d.s1 = s; }
+      m -= st;
+    }
+    st >>= 1;
   }
-  c->rand = r;
+  d.key1 = d.s1 >= 0 ? c->cand_key[d.s1] : INF_BITS;
+  d.key2 = d.s2 >= 0 ? c->cand_key[d.s2] : 0u;
+  d.w = window_of(d.k1, d.s2 >= 0 ? (uint64_t)d.k2 : sp.n, sp, H);
+  d.ok = d.s2 >= 0 && d.key2 >= efk;
+  return d;
 }
 
 // The last CTA runs the scalar control on a shared-memory copy of the control block (one
@@ -1594,7 +1646,13 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   // the stream was finishing; nothing it wrote (nor anything before it) is read before this wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ uint64_t bar_t;  // thread 0: target of the next grid barrier (shared: keeps it out of registers)
-  if (tid == 0) bar_t = grid_sync_base(f.bar);
+  __shared__ uint64_t s_H;    // Alg. 1 l.27's random source for this call (window_hash)
+  __shared__ int s_fast;      // the fast search's single pass took the selection's inputs from fast_walk
+  if (tid == 0) {
+    s_fast = 0;
+    bar_t = grid_sync_base(f.bar);
+    s_H = window_hash(f.sp.seed, f.step, f.sp.rank);
+  }
   if (lane == 0) g_es.run[warp] = warp_run_of(f.sp, blockIdx.x * WARPS + warp);
 #ifdef TK_PHASE_TRACE
   if (tid == 0 && blockIdx.x < 2048) {
@@ -1862,6 +1920,22 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       if (hist) hist_to_counts(tot_p, lev, s_tot);
       else load_totals(tot_p, 16, s_tot);
       if (fast) stamp();
+      if (SEL == SEL_MSTOPK && fast && single && !f.exact_counts) {
+        // the single pass resolved all N levels: the selection's inputs come from fast_walk (every
+        // thread, no serial replay on the critical path); block 0 replays the log after selecting
+        const FastDecision fd = fast_walk(&sc, s_tot, lev, f.sp, efk, s_H);
+        if (tid == 0 && fd.ok) {
+          sc.k1 = fd.k1; sc.k2 = fd.k2; sc.key1 = fd.key1; sc.key2 = fd.key2;
+          sc.prov1 = fd.s1 >= 0 ? p * TMAX + fd.s1 : -1;
+          sc.prov2 = p * TMAX + fd.s2;
+          sc.len2 = fd.w.len2; sc.need = (uint32_t)fd.w.need; sc.rand = fd.w.rand;
+        }
+        if (fd.ok) {
+          s_fast = 1;  // (uniform: every thread took the same decision)
+          stamp();
+          return p + 1;
+        }
+      }
       if (tid == 0) {
         const double cmp_ratio = sc.cmp_ratio;
         s_got = replay_levels<SEL>(&sc, s_tot, min(lev, N - done), p, f.sp.k);
@@ -1870,7 +1944,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
           // key: the bracket's lower end must have reached its coordinate, and nothing overflowed
           sc.cap_ok = (bracket_low_at_least<SEL>(&sc, cmp_ratio) && __ldcg(f.flags) != f.seq) ? 1u : 0u;
         }
-        if (done + s_got == N) finish_window(&sc, f.sp);
+        if (done + s_got == N) finish_window(&sc, f.sp, s_H);
       }
       __syncthreads();
       if (fast) stamp();
@@ -1889,6 +1963,9 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
     if (tid == 0) { sc.cap_ok = 1u; sc.cmp_bottom = 1u; }
     __syncthreads();
     pnext = search(0, true);
+    if (s_fast) {
+      ok = true;
+    } else {
     if (tid == 0) {
       s_got = (sc.prov2 >= 0 && sc.key2 >= efk) ? 1 : 0;  // the search was exact (see above)
       uint64_t lb = 0;
@@ -1898,6 +1975,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
     }
     __syncthreads();
     ok = s_got != 0;
+    }
   }
   if (!ok) {
     if (tid == 0) {
@@ -2095,6 +2173,19 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
         uint32_t t = 0;
         for (int w = 0; w < WARPS; ++w) t += s_w[0][w];
         sc.n_compacted = t;
+      }
+    }
+    if constexpr (SEL == SEL_MSTOPK) {
+      if (s_fast && tid == 0) {
+        // the fast path selected from fast_walk's decisions: Alg. 1's trial log, thresholds and
+        // bracket for the control block, by the same replay (identical decisions and results)
+        search_reset<SEL>(&sc, f.sp.n);
+        replay_levels<SEL>(&sc, s_tot, (int)f.n_iters, 0, f.sp.k);
+        finish_window(&sc, f.sp, s_H);
+        uint64_t lb = 0;
+        for (uint32_t i = 0; i < sc.it && i < (uint32_t)NMAX; ++i)
+          if (sc.key_log[i] < efk) lb |= 1ull << i;
+        sc.nnz_lb = lb;
       }
     }
     ctrl_to_global(f.c, &sc);
