@@ -410,6 +410,25 @@ def extra_configs(a, tk, stream, gs, dev):
         res["C1_phases_us"] = [round(x, 2) for x in c1.stats().phase_us]
         c1.close()
         del g1
+        # C2 k_compress back to back: tk_compress calls on fresh gradients with the residual carried,
+        # CUDA events around the whole loop only (no event between launches, so consecutive
+        # launches overlap through programmatic dependent launch as they do inside a step)
+        c = tk.Context(a.d, rho=a.rho, n_iters=a.n_iters, stream=stream, device=dev)
+        r = torch.zeros(a.d, device="cuda")
+        cidx = torch.empty(c.k, dtype=torch.int32, device="cuda")
+        cval = torch.empty(c.k, device="cuda")
+        for i in range(20):
+            c.compress(gs[i % len(gs)], r, cidx, cval)
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for i in range(100):
+            c.compress(gs[i % len(gs)], r, cidx, cval)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res["C2_compress_back_to_back_us"] = e0.elapsed_time(e1) * 1e3 / 100
+        c.close()
+        del r
         # first call / restart at C2 (median of 3 fresh contexts / 3 forced restarts)
         first, restart, whole = [], [], []
         for rep in range(3):
@@ -449,7 +468,9 @@ def extra_configs(a, tk, stream, gs, dev):
             res[f"C2_{sel}_step_us"] = steps_us(c, gs, 20, torch.zeros(a.d, device="cuda"))
             c.close()
     res["note"] = ("device time per call / step (CUDA events, fresh gradients); C1 replays 16 tk_compress calls "
-                   "per CUDA graph; prose = TK_SELECT_PROSE (P:148), exact = TK_SELECT_EXACT (Eq. 2)")
+                   "per CUDA graph; C2_compress_back_to_back: 100 tk_compress calls between two events (the "
+                   "roofline's per-launch events sit inside the steps instead); prose = TK_SELECT_PROSE (P:148), "
+                   "exact = TK_SELECT_EXACT (Eq. 2)")
     return res
 
 
