@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="tk", choices=["tk", "reference"])
-    ap.add_argument("--d", type=int, default=25_600_000)
+    ap.add_argument("--d", "--dim", dest="d", type=int, default=25_600_000)
     ap.add_argument("--rho", type=float, default=0.001)
     ap.add_argument("--n-iters", type=int, default=10)
     ap.add_argument("--dist", default="G")
