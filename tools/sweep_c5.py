@@ -12,7 +12,7 @@ import paper_2010_10458_b200 as tk
 
 SIZES = [262_144, 1_000_000, 4_000_000, 16_000_000, 25_600_000, 64_000_000, 110_000_000, 134_217_728, 336_000_000]
 RHOS = [1e-4, 1e-3, 1e-2]
-NS = [5, 10, 20]
+NS = [5, 10, 20, 30]
 out = open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/c5_sweep.jsonl", "w")
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
