@@ -181,6 +181,51 @@ __global__ void d_inter(const float* __restrict__ g, float* r, uint64_t n, uint3
   if (tot == 1.2345) g_sink = tot;
 }
 
+// E: the persistent warp-slab layout with the fp64 tree (as k_compress's EF pass) plus a TMA bulk
+// prefetch into L2 of the units PF ahead (g and r, 2 KB each, issued by lane 0; no registers held)
+template <int PF>
+__global__ void e_slab_pf(const float* __restrict__ g, float* r, uint64_t n, uint32_t upw) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const uint64_t u0 = w * upw;
+  const uint64_t nu = n / 512;
+  const uint32_t nun = u0 >= nu ? 0u : (uint32_t)min((uint64_t)upw, nu - u0);
+  auto pf = [&](uint32_t i) {
+    if (lane == 0 && i < nun) {
+      const uint64_t b = (u0 + i) * 512;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g + b), "r"(2048) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(r + b), "r"(2048) : "memory");
+    }
+  };
+  for (int q = 1; q <= PF; ++q) pf(q);
+  double tot = 0.0;
+  for (uint32_t i = 0; i < nun; ++i) {
+    pf(i + PF + 1);
+    const uint64_t base = (u0 + i) * 512 + 4 * lane;
+    float4 gv[4], rv[4], a[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      gv[c] = __ldcs(reinterpret_cast<const float4*>(g + base + c * 128));
+      rv[c] = __ldcs(reinterpret_cast<const float4*>(r + base + c * 128));
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) a[c] = add4(gv[c], rv[c]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) __stcs(reinterpret_cast<float4*>(r + base + c * 128), a[c]);
+    double cs[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double sm = __dadd_rn(__dadd_rn((double)fabsf(a[c].x), (double)fabsf(a[c].y)),
+                            __dadd_rn((double)fabsf(a[c].z), (double)fabsf(a[c].w)));
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) sm = __dadd_rn(sm, __shfl_xor_sync(0xffffffffu, sm, off));
+      cs[c] = sm;
+    }
+    tot = __dadd_rn(tot, __dadd_rn(__dadd_rn(cs[0], cs[1]), __dadd_rn(cs[2], cs[3])));
+  }
+  if (tot == 1.2345) g_sink = tot;
+}
+
 int main(int argc, char** argv) {
   uint64_t n = argc > 1 ? strtoull(argv[1], 0, 10) : 25600000ull;
   const int NB = 6;  // rotate through fresh (g, r) pairs: 6 x 205 MB, beyond L2
@@ -252,6 +297,18 @@ int main(int argc, char** argv) {
       cudaFuncSetAttribute(c_tma<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 6 * 4096);
       timeit(nm, [&](float* gg, float* rr) { c_tma<6, true><<<sms * occ, 256, 8 * 6 * 4096>>>(gg, rr, n, upw); });
     }
+  }
+  for (int occ : {3}) {
+    const uint64_t W = (uint64_t)sms * occ * 8;
+    const uint32_t upw = (uint32_t)((nu + W - 1) / W);
+    snprintf(nm, 96, "slab d1 tree %dx%d (again)", sms, occ);
+    timeit(nm, [&](float* gg, float* rr) { b_slab<1, true><<<sms * occ, 256>>>(gg, rr, n, upw); });
+    snprintf(nm, 96, "slab tree + L2 prefetch +1 %dx%d", sms, occ);
+    timeit(nm, [&](float* gg, float* rr) { e_slab_pf<0><<<sms * occ, 256>>>(gg, rr, n, upw); });
+    snprintf(nm, 96, "slab tree + L2 prefetch +2 %dx%d", sms, occ);
+    timeit(nm, [&](float* gg, float* rr) { e_slab_pf<1><<<sms * occ, 256>>>(gg, rr, n, upw); });
+    snprintf(nm, 96, "slab tree + L2 prefetch +4 %dx%d", sms, occ);
+    timeit(nm, [&](float* gg, float* rr) { e_slab_pf<3><<<sms * occ, 256>>>(gg, rr, n, upw); });
   }
   return 0;
 }
