@@ -303,13 +303,16 @@ def run_reference(a, ws, rank, emit):
 
 
 # ------------------------------------------------------------------------------------------ libtk arm
-def stage_bytes(name, L, d, k, P, ef, chunks):
+def stage_bytes(name, L, d, k, P, ef, chunks, fused_out=False):
     """Algorithmic HBM bytes of ONE launch of a stage."""
     if name == "k_compress":
         # the floor of any correct implementation: the EF pass (read g, read r, write acc - or read
         # g without EF), the k (index, value) pairs and the k residual writes.  This design moves
-        # only that plus the compacted entries (~0.4 % of n, data dependent, not counted)
-        return (12 if ef else 4) * L + 8 * k + (4 * k if ef else 0)
+        # only that plus the compacted entries (~0.4 % of n, data dependent, not counted).  Flat
+        # tk_step without the fused update: the kernel also zeroes the dense aggregate (4 B/element)
+        # and at P = 1 writes its k values (4 B/pair) - there is no decompression then.
+        return ((12 if ef else 4) * L + 8 * k + (4 * k if ef else 0) +
+                ((4 * L + 4 * k) if fused_out else 0))
     if name == "k_decompress":
         return 4 * d + 8 * chunks * k
     if name == "k_tile_ranges":
@@ -597,7 +600,8 @@ def main():
     compute = {kname: v for kname, v in stages.items() if kname.startswith("k_")}
     dom = max(compute, key=lambda kn: compute[kn]["ms_per_launch"] * compute[kn]["launches_per_step"])
     peak, peak_src = measured_hbm()
-    bytes_launch = stage_bytes(dom, L, a.d, k, P, True, chunks)
+    fused_out = n == 1 and P == 1 and not a.sgd  # P = 1 tk_step: k_compress writes the aggregate whole
+    bytes_launch = stage_bytes(dom, L, a.d, k, P, True, chunks, fused_out)
     achieved = bytes_launch / (stages[dom]["ms_per_launch"] * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -616,8 +620,12 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_launch,
                 "ms_per_launch": stages[dom]["ms_per_launch"],
-                "note": "achieved = algorithmic bytes per launch (the floor: 12 B/elem (EF: read g, r; write acc) "
-                        "+ 12 B/pair) / mean CUDA-event duration of that launch inside the profiled steps"}
+                "note": ("achieved = algorithmic bytes per launch (the floor: " +
+                         (("16 B/elem (EF: read g, r; write acc; write the dense aggregate, which at P = 1 this "
+                           "kernel writes) + 16 B/pair" if P == 1 else
+                           "16 B/elem (EF: read g, r; write acc; zero the dense aggregate) + 12 B/pair") if fused_out else
+                          "12 B/elem (EF: read g, r; write acc) + 12 B/pair") +
+                         ") / mean CUDA-event duration of that launch inside the profiled steps")}
 
     nvlink = nvlink_report(a, stages, P, n, L, k, t_step, ctx.chunk_words)
     # comparator: the dense all-reduce of the whole fp32 gradient the sparse path replaces (the paper's

@@ -222,7 +222,8 @@ const void* compress_kernel(bool ef, int np, uint32_t sel) {
 // cooperative launch of k_compress.  With peers != nullptr the gradient is the ordered sum of the
 // np peer segments (HiTopKComm step 1).
 tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, float* val, const Peers* peers = nullptr,
-                        int np = 0, const PushOut* push = nullptr, uint16_t* val16 = nullptr) {
+                        int np = 0, const PushOut* push = nullptr, uint16_t* val16 = nullptr,
+                        float* out_dense = nullptr, bool out_values = false) {
   const bool ef = c->cfg.error_feedback != 0;
   Fused f;
   memset(&f, 0, sizeof(f));
@@ -252,6 +253,8 @@ tk_status compress_impl(tk_ctx* c, const float* g, float* r, uint32_t* idx, floa
   f.val16_out = val16;
   f.wire16 = c->cfg.wire == TK_WIRE_F16 ? 1u : 0u;
   if (push) f.push = *push;
+  f.out_dense = out_dense;
+  f.out_values = out_values ? 1u : 0u;
   f.c = c->ctrl;
   f.step = c->step;
   f.n_iters = c->cfg.n_iters;
@@ -746,10 +749,15 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
       TaggedChunks src{c->pg + parity * stride, c->k, po.tag, c->dev_err, c->timeout_ns};
       TK_TRY(decompress_impl(c, src, c->P, c->k, c->d, out, gat, w, lr));
     } else {
-      TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, co.val, nullptr, 0, nullptr, co.val16));
+      // P = 1 without the fused update: the aggregate of one chunk is the selection itself (Alg. 2
+      // l.15-20: out = +0; out[idx] += val), so the compression writes it whole (zeros after its last
+      // grid barrier, fenced, then the k values) and no decompression runs
+      const bool fuse_out = c->P == 1 && !w && out;
+      TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, co.val, nullptr, 0, nullptr, co.val16,
+                           fuse_out ? out : nullptr, fuse_out));
       if (c->P > 1) TK_NCCL(c, ncclAllGather(mine, gat, c->cw, ncclUint32, c->world, c->stream));
       mark(c, TK_STAGE_ALLGATHER);
-      TK_TRY(decompress_plain(c, gat, c->P, c->d, out, w, lr));
+      if (!fuse_out) TK_TRY(decompress_plain(c, gat, c->P, c->d, out, w, lr));
     }
   } else {
     // HiTopKComm (Alg. 2).  The compressed segment goes straight into this GPU's slot (its node

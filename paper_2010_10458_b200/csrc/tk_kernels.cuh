@@ -1326,6 +1326,7 @@ struct SelOut {
   float* val;       // fp32 value sent (optional)
   uint16_t* val16;  // binary16 value sent (optional; FP16 wire)
   float* r;         // residual write-back (EF; nullptr without)
+  float* out;       // P = 1: the dense aggregate (Alg. 2 l.15-20 with one chunk: out[i] = +0 + sent)
   uint32_t w16;
 };
 
@@ -1339,6 +1340,7 @@ __device__ __forceinline__ void put_sel(const SelOut& o, uint32_t pos, uint32_t 
   }
   if (o.val) o.val[pos] = sent;
   if (o.r) o.r[i] = o.w16 ? __fsub_rn(v, sent) : 0.0f;
+  if (o.out) o.out[i] = __fadd_rn(0.0f, sent);
 }
 
 __device__ __forceinline__ void select_phase(const float* __restrict__ acc, const Ctrl* c, const SearchParams sp,
@@ -1547,6 +1549,9 @@ struct Fused {
   uint16_t* val16_out;       // FP16 wire: binary16 values of the selection (nullptr: none)
   uint32_t* cta_suffix;      // [grid][HIST_BINS] per-CTA histogram suffix sums (barrier-free prefix)
   uint32_t wire16;           // FP16 wire values (F3): round the values sent, keep the error in r
+  float* out_dense;          // P = 1 tk_step without the fused update: the dense aggregate, which this
+                             // kernel writes whole (zeros after its last grid barrier, then the k values)
+  uint32_t out_values;       // 1: the selection writes the values into out_dense (P = 1; no decompression)
 };
 
 // Grid-wide barrier (the launch is cooperative: every CTA is resident) on a monotonic 64-bit
@@ -1648,8 +1653,10 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   __shared__ uint64_t bar_t;  // thread 0: target of the next grid barrier (shared: keeps it out of registers)
   __shared__ uint64_t s_H;    // Alg. 1 l.27's random source for this call (window_hash)
   __shared__ int s_fast;      // the fast search's single pass took the selection's inputs from fast_walk
+  __shared__ int s_zeroed;    // the dense aggregate's zeros were issued (flat tk_step)
   if (tid == 0) {
     s_fast = 0;
+    s_zeroed = 0;
     bar_t = grid_sync_base(f.bar);
     s_H = window_hash(f.sp.seed, f.step, f.sp.rank);
   }
@@ -1662,6 +1669,22 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   }
 #endif
   ctrl_to_smem(&sc, f.c);  // previous call's final state (bracket prediction)  (syncs the CTA)
+  // Flat tk_step without the fused update: the dense aggregate (Alg. 2 l.15-20: +0 everywhere, then
+  // the rank-ordered sums of the pairs) gets its zeros from this kernel, after its LAST grid barrier
+  // (a barrier's release would wait for them) while HBM would otherwise idle through the rest of the
+  // search and the selection.  Each warp zeroes its own slab, where its selection writes the values
+  // afterwards (same warp: program order, __syncwarp and the CTA barriers in between order them).
+  auto zero_out = [&]() {
+    uint64_t zlo, zhi;
+    warp_slab(f.sp, warp, zlo, zhi);
+    float* o = f.out_dense;
+    const uint64_t a4 = min(zhi, (uint64_t)((zlo + 3) & ~(uint64_t)3)), b4 = max(a4, (uint64_t)(zhi & ~(uint64_t)3));
+    for (uint64_t i = zlo + lane; i < a4; i += 32) o[i] = 0.0f;
+#pragma unroll 4
+    for (uint64_t i = a4 + 4 * lane; i < b4; i += 128) __stcs(reinterpret_cast<float4*>(o + i), make_float4(0.f, 0.f, 0.f, 0.f));
+    for (uint64_t i = b4 + lane; i < zhi; i += 32) o[i] = 0.0f;
+    __syncwarp();
+  };
   int nph = 0;
   auto gsync = [&]() __attribute__((always_inline)) {
 #ifdef TK_PHASE_TRACE
@@ -1917,6 +1940,11 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
       }
       gsync();
       stamp();
+      // the fast single pass's barrier is the last one when its decision holds (nearly always)
+      if (f.out_dense && fast && single && SEL == SEL_MSTOPK && !f.exact_counts) {
+        zero_out();
+        if (tid == 0) s_zeroed = 1;  // read before the prefix, after several CTA barriers
+      }
       if (hist) hist_to_counts(tot_p, lev, s_tot);
       else load_totals(tot_p, 16, s_tot);
       if (fast) stamp();
@@ -2052,6 +2080,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
   const uint32_t W = f.sp.W;
   uint64_t slo, shi;
   warp_slab(f.sp, warp, slo, shi);
+  if (f.out_dense && !s_zeroed) zero_out();  // (s_zeroed is uniform here: set before a CTA barrier, never after)
   uint32_t c1 = 0, call = 0;
   if (lane == 0) s_ne[warp] = 0u;
   if (sc.cap_ok) {
@@ -2136,6 +2165,7 @@ __global__ void __launch_bounds__(THREADS, TK_MIN_BLOCKS) k_compress(Fused f) {
     so.val = f.val_out;
     so.val16 = f.val16_out;
     so.r = EF ? f.r : nullptr;
+    so.out = f.out_values ? f.out_dense : nullptr;
     so.w16 = f.wire16;
     select_phase(f.acc, &sc, f.sp, c1, c2, b1, b2, so, f.cp);
   }
