@@ -308,9 +308,9 @@ def stage_bytes(name, L, d, k, P, ef, chunks, fused_out=False):
     if name == "k_compress":
         # the floor of any correct implementation: the EF pass (read g, read r, write acc - or read
         # g without EF), the k (index, value) pairs and the k residual writes.  This design moves
-        # only that plus the compacted entries (~0.4 % of n, data dependent, not counted).  Flat
-        # tk_step without the fused update: the kernel also zeroes the dense aggregate (4 B/element)
-        # and at P = 1 writes its k values (4 B/pair) - there is no decompression then.
+        # only that plus the compacted entries (~0.4 % of n, data dependent, not counted).  P = 1
+        # tk_step without the fused update: the kernel also writes the dense aggregate (its zeros,
+        # 4 B/element, and its k values, 4 B/pair) - there is no decompression then.
         return ((12 if ef else 4) * L + 8 * k + (4 * k if ef else 0) +
                 ((4 * L + 4 * k) if fused_out else 0))
     if name == "k_decompress":
@@ -621,9 +621,8 @@ def main():
                 "algorithmic_bytes_per_launch": bytes_launch,
                 "ms_per_launch": stages[dom]["ms_per_launch"],
                 "note": ("achieved = algorithmic bytes per launch (the floor: " +
-                         (("16 B/elem (EF: read g, r; write acc; write the dense aggregate, which at P = 1 this "
-                           "kernel writes) + 16 B/pair" if P == 1 else
-                           "16 B/elem (EF: read g, r; write acc; zero the dense aggregate) + 12 B/pair") if fused_out else
+                         ("16 B/elem (EF: read g, r; write acc; write the dense aggregate, which at P = 1 this "
+                          "kernel writes) + 16 B/pair" if fused_out else
                           "12 B/elem (EF: read g, r; write acc) + 12 B/pair") +
                          ") / mean CUDA-event duration of that launch inside the profiled steps")}
 

@@ -751,7 +751,7 @@ static tk_status step_impl(tk_ctx* c, const float* g, float* r, float* out, uint
     } else {
       // P = 1 without the fused update: the aggregate of one chunk is the selection itself (Alg. 2
       // l.15-20: out = +0; out[idx] += val), so the compression writes it whole (zeros after its last
-      // grid barrier, fenced, then the k values) and no decompression runs
+      // grid barrier, then the k values, each warp over its own slab) and no decompression runs
       const bool fuse_out = c->P == 1 && !w && out;
       TK_TRY(compress_impl(c, g, ef ? r : nullptr, mine, co.val, nullptr, 0, nullptr, co.val16,
                            fuse_out ? out : nullptr, fuse_out));
