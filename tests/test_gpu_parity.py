@@ -198,6 +198,29 @@ def test_flat_step_single_rank(tk, d, rho, dist):
         r = ref.per_rank[0].residual
 
 
+@pytest.mark.parametrize("d,rho,dist", [(3_000_017, 0.01, "L"), (3_000_017, 0.01, "G"), (1_000_000, 0.001, "G")])
+def test_step_p1_writes_every_element_of_out(tk, d, rho, dist):
+    """At P = 1 tk_step's k_compress writes the whole aggregate (Alg. 2 l.15-20 with one chunk: +0,
+    then the k values) and no decompression runs: every element of out must be written, whatever out
+    held before (a NaN pattern here) - on the first call (whole-vector search) and on later calls
+    (the fast search).  Guards the round-2 race in which late warps skipped zeroing their slab."""
+    k = oracle.k_from_density(d, rho)
+    ctx = tk.Context(d, rho=rho, n_iters=10, seed=3)
+    r = np.zeros(d, np.float32)
+    rd = _dev(r)
+    for step in range(4):
+        g = gradgen.gradient(d, dist, cfg=32, step=step)
+        out = torch.full((d,), float("nan"), device="cuda")
+        gat = torch.empty(2 * k, dtype=torch.int32, device="cuda")
+        ctx.step(_dev(g), rd, out=out, gathered=gat)
+        ref = oracle.flat_step([g], [r], rho, 10, seed=3, step=step)
+        assert np.array_equal(_u32(gat), ref.gathered), step
+        assert np.array_equal(_f32bits(out), ref.out.view(np.uint32)), step
+        assert np.array_equal(_f32bits(rd), ref.per_rank[0].residual.view(np.uint32)), step
+        r = ref.per_rank[0].residual
+    ctx.close()
+
+
 def test_step_host_matches_device_path(tk):
     d, rho = 500_000, 0.001
     ctx = tk.Context(d, rho=rho, n_iters=10, seed=8)
