@@ -208,7 +208,7 @@ def test_step_p1_writes_every_element_of_out(tk, d, rho, dist):
     ctx = tk.Context(d, rho=rho, n_iters=10, seed=3)
     r = np.zeros(d, np.float32)
     rd = _dev(r)
-    for step in range(4):
+    for step in range(8):
         g = gradgen.gradient(d, dist, cfg=32, step=step)
         out = torch.full((d,), float("nan"), device="cuda")
         gat = torch.empty(2 * k, dtype=torch.int32, device="cuda")
