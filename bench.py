@@ -707,8 +707,8 @@ def main():
                            "levels_per_pass": a.levels or 10, "input_buffers": nbuf,
                            "inputs": "fresh seeded N(0,1) gradient per step (torch CUDA generator, pre-generated in "
                                      "HBM); residual carried from r=0 at step 0; timed steps W..W+K-1",
-                           "l2": "inputs larger than L2: each step reads a fresh g (4d B) and touches r and out: "
-                                 f"{12 * a.d / 1e6:.0f} MB per rank per step vs 126 MB L2; no explicit flush"},
+                           "l2": "inputs larger than L2: each step reads a fresh g (4d B), reads and writes r and "
+                                 f"writes out: {16 * a.d / 1e6:.0f} MB per rank per step vs 126 MB L2; no explicit flush"},
                 "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "stages": stages, "recall_vs_exact": recall, "nvlink": nvlink,
                 "dense_allreduce_comparator": allreduce, "extra_configs": extra}
